@@ -1,0 +1,249 @@
+/*
+ * autoshard_b200.h — C-ABI of the B200-native AutoShard embedding-bag hot path.
+ *
+ * This is the drop-in boundary. Everything is plain C: POD
+ * structs, raw pointers and sizes, status codes, no exceptions and no torch
+ * types. The C++ header autoshard_b200.hpp wraps it back into the reference's
+ * own C++ shapes (autoshard::gpu::measure_plan etc.).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths under /root/reference/proj/include/autoshard/).
+ *
+ * Threading: an as_ctx is bound to one CUDA device and is not thread-safe;
+ * use one host thread (or process) per device. Host-side generator / planner
+ * calls are pure and reentrant. Errors: every call returns an as_status; the
+ * message of the last failure on the calling thread is as_last_error().
+ */
+#ifndef AUTOSHARD_B200_H
+#define AUTOSHARD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AS_API __attribute__((visibility("default")))
+#else
+#define AS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mirrors the exception taxonomy of common.hpp:15-50 (+ device failures). */
+typedef enum as_status {
+  AS_OK = 0,
+  AS_CONFIG = 1,     /* ConfigError */
+  AS_PARSE = 2,      /* ParseError */
+  AS_OFFSET = 3,     /* OffsetError (ParseError subclass) */
+  AS_INDEX = 4,      /* IndexError (ParseError subclass) */
+  AS_INFEASIBLE = 5, /* InfeasibleError */
+  AS_SHAPE = 6,      /* ShapeError */
+  AS_LOOKUP = 7,     /* LookupError */
+  AS_GUARD = 8,      /* GuardError */
+  AS_STATE = 9,      /* StateError */
+  AS_CUDA = 10,      /* CUDA runtime / launch failure */
+  AS_NCCL = 11       /* collective failure */
+} as_status;
+
+/* TableDesc, tables.hpp:24-38. Same field order/meaning. */
+typedef struct as_table_spec {
+  int32_t id;
+  int32_t dim;              /* embedding length; device path needs dim % 4 == 0, 4..1024 */
+  int64_t hash_size;        /* rows */
+  double pooling_mean;      /* declared mean lookups per query */
+  double access_ratio;      /* fraction of rows ever accessed */
+  int32_t bytes_per_param;  /* planning size only (size_bytes); device stores fp32 */
+  int32_t _pad;
+} as_table_spec;
+
+/* GeneratorConfig, tables.hpp:149-174. */
+typedef struct as_generator_config {
+  double hash_size_min, hash_size_max;
+  double pooling_mean_target, pooling_shape, pooling_cap;
+  const int32_t* dim_choices;
+  int32_t n_dim_choices;
+  double access_ratio_min, access_ratio_max;
+  int32_t bytes_per_param;
+} as_generator_config;
+
+/* BenchConfig, simcost.hpp:163-171, plus the GPU-only knobs. */
+typedef struct as_bench_config {
+  int32_t warmup;   /* W (default 5) */
+  int32_t measure;  /* B (default 10) */
+  int32_t trim;     /* R (default 2); needs measure - 2*trim >= 1 */
+  int32_t flush_l2; /* overwrite a buffer of 2x L2 before each measured run */
+  uint64_t seed;    /* weight-init seed of the measured contexts */
+  float lr, eps;    /* row-wise Adagrad hyper-parameters of the measured step */
+} as_bench_config;
+
+typedef struct as_workload as_workload; /* host-side Workload (tables.hpp:43-60) */
+typedef struct as_ctx as_ctx;           /* one device, one shard of tables */
+
+AS_API const char* as_version(void);
+AS_API const char* as_last_error(void);
+
+/* ---------------------------------------------------------------------- */
+/* L1 — synthetic tables and streams (tables.hpp, workload_io.hpp)        */
+/* ---------------------------------------------------------------------- */
+
+/* GeneratorConfig{} defaults; dim_choices points at static {16, 32}. */
+AS_API void as_generator_config_default(as_generator_config* cfg);
+
+/* generate_pool, tables.hpp:178-200 (bit-exact). out has n entries. */
+AS_API as_status as_generate_pool(uint64_t seed, int32_t n_tables, const as_generator_config* cfg,
+                                  as_table_spec* out);
+
+/* generate_workload, tables.hpp:237-288 (bit-exact; tables processed in
+ * parallel on n_threads host threads, 0 = all cores). */
+AS_API as_status as_generate_workload(uint64_t seed, const as_table_spec* tables, int32_t n_tables,
+                                      int64_t batch_size, double zipf_exponent, int32_t n_threads,
+                                      as_workload** out);
+
+/* Workload::find (tables.hpp:53-59) and accessors; pointers owned by wl. */
+AS_API int64_t as_workload_batch_size(const as_workload* wl);
+AS_API int32_t as_workload_num_tables(const as_workload* wl);
+AS_API as_status as_workload_stream(const as_workload* wl, int32_t i, int32_t* table_id,
+                                    const int64_t** offsets, const int64_t** indices,
+                                    int64_t* n_indices);
+AS_API as_status as_workload_find(const as_workload* wl, int32_t table_id, int32_t* position);
+/* Build a workload from caller arrays (copied). offsets[i] has batch+1 entries. */
+AS_API as_status as_workload_from_arrays(int64_t batch_size, int32_t n_tables,
+                                         const int32_t* table_ids, const int64_t* const* offsets,
+                                         const int64_t* const* indices, const int64_t* n_indices,
+                                         as_workload** out);
+/* Page-lock the stream buffers (cudaHostRegister) so device loads run at full
+ * PCIe rate; undone by as_workload_destroy. */
+AS_API as_status as_workload_pin(as_workload* wl);
+AS_API void as_workload_destroy(as_workload* wl);
+
+/* save_workload / load_workload (workload_io.hpp:151-245): same file format,
+ * same validation and error classes (OffsetError / IndexError naming the table). */
+AS_API as_status as_workload_save(const as_workload* wl, const as_table_spec* tables,
+                                  const char* path);
+/* tables_out: capacity max_tables; n_tables receives the count. */
+AS_API as_status as_workload_load(const char* path, as_workload** out, as_table_spec* tables_out,
+                                  int32_t max_tables, int32_t* n_tables);
+AS_API as_status as_pool_save(const as_table_spec* tables, int32_t n, const char* path);
+AS_API as_status as_pool_load(const char* path, as_table_spec* tables_out, int32_t max_tables,
+                              int32_t* n_tables);
+
+/* fingerprint(pool) / fingerprint(ShardingTask), tables.hpp:417-441. */
+AS_API uint64_t as_fingerprint_pool(const as_table_spec* tables, int32_t n);
+AS_API uint64_t as_fingerprint_task(const as_table_spec* tables, int32_t n, int32_t num_shards,
+                                    const int64_t* mem_budget);
+
+/* ---------------------------------------------------------------------- */
+/* L3 — plans (tables.hpp:63-143, planners.hpp, SPEC.md:291 plan file)    */
+/* ---------------------------------------------------------------------- */
+
+/* kind: 0 size-greedy, 1 dim-greedy, 2 lookup-greedy (HeuristicKind, planners.hpp:20). */
+AS_API as_status as_heuristic_cost(const as_table_spec* t, int32_t kind, double* cost);
+AS_API as_status as_greedy_shard(const as_table_spec* tables, int32_t n, int32_t num_shards,
+                                 const int64_t* mem_budget, int32_t kind, int32_t* assignment);
+AS_API as_status as_random_shard(const as_table_spec* tables, int32_t n, int32_t num_shards,
+                                 const int64_t* mem_budget, uint64_t seed, int32_t* assignment);
+/* ShardingPlan::validate / mem_used / feasible. */
+AS_API as_status as_plan_validate(int32_t n, int32_t num_shards, const int32_t* assignment);
+AS_API as_status as_plan_mem_used(const as_table_spec* tables, int32_t n, int32_t num_shards,
+                                  const int32_t* assignment, int64_t* used);
+AS_API as_status as_degree_of_balance(const double* costs, int32_t n, double* balance);
+/* Plan file: "autoshard-plan 1", task fingerprint, assignment, optional costs. */
+AS_API as_status as_plan_save(const char* path, const as_table_spec* tables, int32_t n,
+                              int32_t num_shards, const int64_t* mem_budget,
+                              const int32_t* assignment, const double* costs_or_null);
+/* Validates the fingerprint against (tables, budgets); costs_out may be NULL. */
+AS_API as_status as_plan_load(const char* path, const as_table_spec* tables, int32_t n,
+                              int32_t num_shards, const int64_t* mem_budget, int32_t* assignment,
+                              double* costs_out, int32_t* has_costs);
+
+/* ---------------------------------------------------------------------- */
+/* L2 — the device hot path (replaces SIM-1/SIM-2, simcost.hpp:60-115)    */
+/* ---------------------------------------------------------------------- */
+
+/* One shard on one device: allocates fp32 tables [hash, dim] (counter-hash
+ * init from weight_seed), fp32 row-wise momentum (0), and
+ * workspaces for batch_size. Tables keep the given order; their pooled
+ * columns are laid out in that order. n_tables may be 0 (empty shard). */
+AS_API as_status as_create(int32_t device, const as_table_spec* tables, int32_t n_tables,
+                           int64_t batch_size, uint64_t weight_seed, as_ctx** out);
+AS_API as_status as_destroy(as_ctx* ctx);
+
+/* Load one batch of streams (host int64 CSR per table, ctx table order,
+ * TableStream layout tables.hpp:43-47). Host memory is borrowed for the call
+ * only. Validation reproduces load_workload's checks (workload_io.hpp:216-241)
+ * on the device and reports OffsetError / IndexError naming the table.
+ * stream: a cudaStream_t (NULL = legacy default). Synchronises. */
+AS_API as_status as_load_streams(as_ctx* ctx, const int64_t* const* offsets,
+                                 const int64_t* const* indices, const int64_t* n_indices,
+                                 void* stream);
+/* Same, picking the ctx's tables from a workload by id (LookupError if absent). */
+AS_API as_status as_load_workload(as_ctx* ctx, const as_workload* wl, void* stream);
+
+/* K4+K1: pooled[b, col_t + d] = sum_{j in bag (t,b)} W_t[idx_j, d]; empty bag -> 0.
+ * out: device [batch, sum_dim] fp32, or NULL for the ctx's own buffer. */
+AS_API as_status as_forward(as_ctx* ctx, float* out_or_null, void* stream);
+
+/* K2+K3: sort (row, bag), segment-sum the gradient rows per unique row and
+ * apply exact row-wise Adagrad in place:
+ *   m_r += |g_r|^2 / dim ;  W_r -= lr * g_r / (sqrt(m_r) + eps).
+ * grad: device [batch, sum_dim] fp32, or NULL = the ctx's pooled output
+ * (loss = 1/2 |pooled|^2). */
+AS_API as_status as_backward_rowwise_adagrad(as_ctx* ctx, const float* grad_or_null, float lr,
+                                             float eps, void* stream);
+
+/* One training step on the loaded batch: forward into the ctx buffer, loss
+ * 1/2 |pooled|^2 (if loss_out != NULL it is computed and copied to host,
+ * which synchronises), backward with grad = pooled. */
+AS_API as_status as_step(as_ctx* ctx, float lr, float eps, double* loss_out, void* stream);
+
+/* Micro-benchmark of this shard (simcost.hpp:140-154 on
+ * real kernels): W warm-up steps, B measured steps (each after an L2 flush
+ * when flush_l2), CUDA-event timed, sorted, R dropped at each end, mean ms. */
+AS_API as_status as_measure(as_ctx* ctx, int32_t warmup, int32_t measure, int32_t trim,
+                            int32_t flush_l2, float lr, float eps, double* ms_out);
+
+/* measure_plan (simcost.hpp:194-204) on the GPU: for shard k a ctx holding
+ * plan's tables is created on devices[k % n_devices], its streams loaded from
+ * wl, and as_measure run; costs[k] in ms. Same validation as the reference
+ * (ConfigError on a bad plan, LookupError on a table absent from wl). */
+AS_API as_status as_measure_plan(const as_table_spec* tables, int32_t n, int32_t num_shards,
+                                 const int32_t* assignment, const as_workload* wl,
+                                 const int32_t* devices, int32_t n_devices,
+                                 const as_bench_config* bench, double* costs);
+
+/* Introspection for hosts that drive collectives themselves. */
+typedef struct as_ctx_info {
+  int32_t device;
+  int32_t n_tables;
+  int64_t batch_size;
+  int64_t sum_dim;       /* pooled row width */
+  int64_t total_rows;    /* sum hash_size */
+  int64_t n_lookups;     /* of the loaded batch (0 before a load) */
+  int64_t n_chunks;      /* work chunks of the loaded batch */
+  int64_t device_bytes;  /* bytes allocated on the device */
+  float* pooled;         /* device [batch, sum_dim] */
+  float* weights;        /* device, concatenated [hash_t, dim_t] */
+  float* momentum;       /* device [total_rows] */
+  int32_t kernels_per_step; /* kernel launches of one as_step */
+  int32_t _pad;
+} as_ctx_info;
+AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info);
+
+/* Readbacks for parity (synchronise). */
+/* rows: n row ids (table-local) of ctx table position t -> out [n, dim] fp32. */
+AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out);
+AS_API as_status as_read_momentum(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n,
+                                  float* out);
+/* what: 0 pooled [batch, sum_dim] fp32; 1 bag id per lookup int32 [n_lookups];
+ *       2 sorted global rows int32 [n_lookups]; 3 sorted bag ids int32;
+ *       4 device index array (global rows) int32 [n_lookups]. */
+AS_API as_status as_read_buffer(as_ctx* ctx, int32_t what, void* host_out, int64_t nbytes);
+/* Overwrite dense table t / momentum from host (tests). */
+AS_API as_status as_write_table(as_ctx* ctx, int32_t t, const float* w_or_null,
+                                const float* m_or_null);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AUTOSHARD_B200_H */

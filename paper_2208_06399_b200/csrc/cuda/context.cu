@@ -1,0 +1,476 @@
+// Device context of one shard on one B200: allocation, counter-hash init,
+// stream loading with on-device validation, forward, backward (sort + segment
+// reduce + row-wise Adagrad) and the micro-benchmark protocol.
+//
+// HBM layout (per context):
+//   W      fp32, tables concatenated in context order, each [hash_t, dim_t] row-major
+//   M      fp32 [sum hash_t]  row-wise Adagrad momentum, indexed by GLOBAL row
+//   idx32  int32 [L]  lookups as GLOBAL rows (row_off_t + idx), table-major
+//   off32  int32 [T*B + 1] rebased bag offsets (TBE layout)
+//   bag    int32 [L]  bag id of each lookup (K4)
+//   skey/sbag int32 [L] lookups sorted by global row (stable), with bag ids
+//   pooled fp32 [B, sum dim_t], table columns in context order
+#include "context.hpp"
+#include "kernels.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+namespace asb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(AS_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != d) cuda_check(cudaSetDevice(d), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int kind_for_dim(int dim) {
+  const int nvec = dim / 4;
+  if (nvec <= 1) return 0;
+  if (nvec <= 2) return 1;
+  if (nvec <= 4) return 2;
+  if (nvec <= 8) return 3;
+  if (nvec <= 16) return 4;
+  if (nvec <= 32) return 5;
+  if (nvec <= 64) return 6;
+  if (nvec <= 128) return 7;
+  return 8;
+}
+
+// Elements per chunk: ~64 KB of gathered rows per warp, multiple of 32.
+int chunk_len_for_dim(int dim) {
+  int c = 65536 / (dim * 4);
+  c = (c / 32) * 32;
+  return std::max(32, std::min(4096, c));
+}
+
+int bit_width_u64(uint64_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ src, long long w_off, int dim,
+                                   const long long* __restrict__ rows, long long n,
+                                   float* __restrict__ dst) {
+  const long long total = n * dim;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long i = q / dim;
+    const int d = (int)(q - i * dim);
+    dst[q] = src[w_off + rows[i] * dim + d];
+  }
+}
+
+constexpr int kBlock = 256;
+constexpr int kWarpsPerBlock = kBlock / 32;
+
+unsigned grid_for(long long work, long long per_block) {
+  long long g = (work + per_block - 1) / per_block;
+  return (unsigned)std::max(1LL, g);
+}
+
+}  // namespace
+
+void* EmbContext::dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 16;
+  cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  bytes_ += static_cast<int64_t>(bytes);
+  allocs_.push_back(p);
+  return p;
+}
+
+EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed)
+    : device_(device), T_(n), B_(batch), seed_(seed) {
+  if (n < 0) fail(AS_CONFIG, "as_create: n_tables must be >= 0");
+  if (batch < 1 || batch > (1LL << 30)) fail(AS_CONFIG, "as_create: batch_size must be in [1, 2^30]");
+  int ndev = 0;
+  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    fail(AS_CONFIG, "as_create: device " + std::to_string(device) + " out of range (" +
+                        std::to_string(ndev) + " visible)");
+  specs_.assign(tables, tables + n);
+  htabs_.resize(static_cast<size_t>(n));
+  int64_t w_off = 0;
+  for (int t = 0; t < n; ++t) {
+    const as_table_spec& s = specs_[t];
+    if (s.dim < 4 || s.dim > 1024 || s.dim % 4 != 0)
+      fail(AS_CONFIG, "table " + std::to_string(s.id) + ": device path needs dim % 4 == 0 and 4 <= dim <= 1024, got " +
+                          std::to_string(s.dim));
+    if (s.hash_size < 1) fail(AS_CONFIG, "table " + std::to_string(s.id) + " has invalid hash_size");
+    DevTable& d = htabs_[t];
+    std::memset(&d, 0, sizeof d);
+    d.row_off = total_rows_;
+    d.w_base = w_off - total_rows_ * s.dim;
+    d.hash = s.hash_size;
+    d.dim = s.dim;
+    d.col = static_cast<int>(sum_dim_);
+    d.table_id = s.id;
+    d.kind = kind_for_dim(s.dim);
+    d.chunk_len = chunk_len_for_dim(s.dim);
+    total_rows_ += s.hash_size;
+    w_off += s.hash_size * s.dim;
+    sum_dim_ += s.dim;
+    max_dim_ = std::max(max_dim_, s.dim);
+  }
+  total_w_ = w_off;
+  if (total_rows_ >= (1LL << 31))
+    fail(AS_SHAPE, "as_create: a shard holds at most 2^31-1 rows (int32 row ids), got " +
+                       std::to_string(total_rows_));
+  end_bit_ = std::max(1, bit_width_u64(static_cast<uint64_t>(std::max<int64_t>(total_rows_ - 1, 0))));
+
+  DeviceGuard g(device_);
+  dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
+  W_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_w_)));
+  M_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_rows_)));
+  out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
+  off32_ = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
+  stage_off_ = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
+  err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
+  loss_ = static_cast<double*>(dalloc(sizeof(double)));
+  int l2 = 0;
+  cuda_check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_), "L2 size");
+  flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
+  flush_ = dalloc(flush_bytes_);
+
+  // K6: weights from the counter hash, momentum zero.
+  const unsigned long long s0 = splitmix64(seed_);
+  int64_t off = 0;
+  for (int t = 0; t < n; ++t) {
+    const long long nv = specs_[t].hash_size * (specs_[t].dim / 4);
+    const unsigned grid = static_cast<unsigned>(std::min<long long>((nv + 255) / 256, 148LL * 64));
+    init_table_kernel<<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
+    off += specs_[t].hash_size * specs_[t].dim;
+  }
+  cuda_check(cudaGetLastError(), "init_table_kernel");
+  cuda_check(cudaMemset(M_, 0, sizeof(float) * static_cast<size_t>(total_rows_)), "momentum init");
+  cuda_check(cudaMemcpy(dtabs_, htabs_.data(), sizeof(DevTable) * n, cudaMemcpyHostToDevice), "tables H2D");
+  cuda_check(cudaDeviceSynchronize(), "init");
+}
+
+EmbContext::~EmbContext() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
+  for (void* p : allocs_) cudaFree(p);
+  if (prev >= 0) cudaSetDevice(prev);
+}
+
+void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks) {
+  auto drop = [this](void* p) {
+    if (!p) return;
+    auto it = std::find(allocs_.begin(), allocs_.end(), p);
+    if (it != allocs_.end()) allocs_.erase(it);
+    cudaFree(p);
+  };
+  if (L > cap_L_) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    for (void* p : {(void*)idx32_, (void*)bag_, (void*)skey_, (void*)sbag_, (void*)stage_idx_, cub_tmp_}) drop(p);
+    const int64_t cap = std::max<int64_t>(L + L / 8, 1024);
+    idx32_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    bag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    skey_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    sbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    stage_idx_ = static_cast<long long*>(dalloc(sizeof(long long) * cap));
+    size_t tmp = 0;
+    cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(nullptr, tmp, (const unsigned*)nullptr, (unsigned*)nullptr,
+                                               (const int*)nullptr, (int*)nullptr, (int)cap, 0, end_bit_),
+               "cub sizing");
+    cub_bytes_ = tmp;
+    cub_tmp_ = dalloc(tmp);
+    cap_L_ = cap;
+  }
+  if (n_chunks > cap_chunks_) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    drop(chunk_table_);
+    drop(carry_);
+    const int64_t cap = std::max<int64_t>(n_chunks + n_chunks / 8, 64);
+    chunk_table_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    carry_ = static_cast<float*>(dalloc(sizeof(float) * cap * 2 * max_dim_));
+    cap_chunks_ = cap;
+  }
+}
+
+void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
+                      cudaStream_t s) {
+  DeviceGuard g(device_);
+  loaded_ = false;
+  int64_t L = 0, nch = 0;
+  for (int t = 0; t < T_; ++t) {
+    if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
+    DevTable& d = htabs_[t];
+    d.idx_off = L;
+    d.n_lookups = n_idx[t];
+    d.chunk_off = static_cast<int>(nch);
+    L += n_idx[t];
+    nch += (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
+  }
+  if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
+  if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
+  ensure_capacity(L, nch);
+  std::vector<int> ctab(static_cast<size_t>(nch));
+  for (int t = 0; t < T_; ++t) {
+    const int64_t n = (htabs_[t].n_lookups + htabs_[t].chunk_len - 1) / htabs_[t].chunk_len;
+    std::fill(ctab.begin() + htabs_[t].chunk_off, ctab.begin() + htabs_[t].chunk_off + n, t);
+  }
+  // H2D: raw int64 CSR into staging (pinned sources run at full PCIe rate).
+  for (int t = 0; t < T_; ++t) {
+    cuda_check(cudaMemcpyAsync(stage_off_ + (int64_t)t * (B_ + 1), offsets[t], sizeof(int64_t) * (B_ + 1),
+                               cudaMemcpyHostToDevice, s),
+               "offsets H2D");
+    if (n_idx[t] > 0)
+      cuda_check(cudaMemcpyAsync(stage_idx_ + htabs_[t].idx_off, indices[t], sizeof(int64_t) * n_idx[t],
+                                 cudaMemcpyHostToDevice, s),
+                 "indices H2D");
+  }
+  if (T_ > 0)
+    cuda_check(cudaMemcpyAsync(dtabs_, htabs_.data(), sizeof(DevTable) * T_, cudaMemcpyHostToDevice, s),
+               "tables H2D");
+  if (nch > 0)
+    cuda_check(cudaMemcpyAsync(chunk_table_, ctab.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s),
+               "chunk table H2D");
+  cuda_check(cudaMemsetAsync(err_, 0xff, sizeof(unsigned long long), s), "err reset");
+  if (T_ > 0) {
+    const long long n = (long long)T_ * (B_ + 1);
+    pack_offsets_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, s>>>(
+        stage_off_, T_, (int)B_, dtabs_, off32_, err_);
+    cuda_check(cudaGetLastError(), "pack_offsets_kernel");
+  }
+  if (nch > 0) {
+    pack_indices_kernel<<<grid_for(nch, kWarpsPerBlock), kBlock, 0, s>>>(stage_idx_, dtabs_, chunk_table_,
+                                                                        (int)nch, idx32_, err_);
+    cuda_check(cudaGetLastError(), "pack_indices_kernel");
+  }
+  unsigned long long err = 0;
+  cuda_check(cudaMemcpyAsync(&err, err_, sizeof err, cudaMemcpyDeviceToHost, s), "err D2H");
+  cuda_check(cudaStreamSynchronize(s), "load sync");
+  if (err != ~0ull) {
+    const int t = static_cast<int>(err >> 42);
+    const int kind = static_cast<int>((err >> 40) & 3);
+    const int64_t q = static_cast<int64_t>(err & ((1ull << 40) - 1));
+    const std::string where = "table " + std::to_string(specs_[t].id);
+    switch (kind) {
+      case 0: fail(AS_OFFSET, where + ": offsets must start at 0, got " + std::to_string(offsets[t][0]));
+      case 1: fail(AS_OFFSET, where + ": offsets must be nondecreasing at entry " + std::to_string(q));
+      case 2:
+        fail(AS_OFFSET, where + ": final offset " + std::to_string(offsets[t][B_]) + " != index count " +
+                            std::to_string(n_idx[t]));
+      default:
+        fail(AS_INDEX, where + ": index " + std::to_string(indices[t][q]) + " out of range [0, " +
+                           std::to_string(specs_[t].hash_size) + ")");
+    }
+  }
+  L_ = L;
+  n_chunks_ = nch;
+  loaded_ = true;
+}
+
+void EmbContext::require_loaded(const char* what) const {
+  if (!loaded_) fail(AS_STATE, std::string(what) + ": no streams loaded (call as_load_streams first)");
+}
+
+SegParams EmbContext::seg_params(bool fwd) const {
+  SegParams p;
+  std::memset(&p, 0, sizeof p);
+  p.tabs = dtabs_;
+  p.chunk_table = chunk_table_;
+  p.n_chunks = static_cast<int>(n_chunks_);
+  p.seg = fwd ? bag_ : skey_;
+  p.src = fwd ? idx32_ : sbag_;
+  p.carry = carry_;
+  p.carry_stride = max_dim_;
+  return p;
+}
+
+void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
+  require_loaded("as_forward");
+  DeviceGuard g(device_);
+  if (T_ == 0) return;
+  float* target = out ? out : out_;
+  const long long nb = (long long)T_ * B_;
+  bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
+                                                                          target, sum_dim_);
+  cuda_check(cudaGetLastError(), "bag_expand_kernel");
+  if (n_chunks_ == 0) return;
+  SegParams p = seg_params(true);
+  p.W_ro = W_;
+  p.out = target;
+  p.out_stride = sum_dim_;
+  p.loss = loss_dev;
+  const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
+  seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "seg_reduce_kernel<fwd>");
+  seg_fixup_kernel<true><<<grid, kBlock, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
+}
+
+void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
+  require_loaded("as_backward_rowwise_adagrad");
+  DeviceGuard g(device_);
+  if (T_ == 0 || n_chunks_ == 0) return;
+  size_t tmp = cub_bytes_;
+  cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_),
+                                             reinterpret_cast<unsigned*>(skey_), bag_, sbag_, (int)L_, 0,
+                                             end_bit_, s),
+             "cub SortPairs");
+  SegParams p = seg_params(false);
+  p.grad = grad ? grad : out_;
+  p.grad_stride = sum_dim_;
+  p.W = W_;
+  p.M = M_;
+  p.lr = lr;
+  p.eps = eps;
+  const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
+  seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "seg_reduce_kernel<bwd>");
+  seg_fixup_kernel<false><<<grid, kBlock, 0, s>>>(p);
+  cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
+}
+
+void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
+  require_loaded("as_step");
+  DeviceGuard g(device_);
+  if (loss_host) cuda_check(cudaMemsetAsync(loss_, 0, sizeof(double), s), "loss reset");
+  forward(out_, loss_host ? loss_ : nullptr, s);
+  backward(out_, lr, eps, s);
+  if (loss_host) {
+    cuda_check(cudaMemcpyAsync(loss_host, loss_, sizeof(double), cudaMemcpyDeviceToHost, s), "loss D2H");
+    cuda_check(cudaStreamSynchronize(s), "step sync");
+  }
+}
+
+double EmbContext::measure(int warmup, int measure, int trim, bool flush, float lr, float eps) {
+  if (warmup < 0 || measure < 1 || trim < 0 || measure - 2 * trim < 1)
+    fail(AS_CONFIG, "micro_benchmark: need measure - 2*trim >= 1, got B=" + std::to_string(measure) +
+                        " R=" + std::to_string(trim));
+  require_loaded("as_measure");
+  DeviceGuard g(device_);
+  cudaStream_t s;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * measure));
+  for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+  for (int i = 0; i < warmup; ++i) step(lr, eps, nullptr, s);
+  for (int i = 0; i < measure; ++i) {
+    if (flush) cuda_check(cudaMemsetAsync(flush_, i & 0xff, flush_bytes_, s), "l2 flush");
+    cuda_check(cudaEventRecord(ev[2 * i], s), "event");
+    step(lr, eps, nullptr, s);
+    cuda_check(cudaEventRecord(ev[2 * i + 1], s), "event");
+  }
+  cuda_check(cudaStreamSynchronize(s), "measure sync");
+  std::vector<double> ms(static_cast<size_t>(measure));
+  for (int i = 0; i < measure; ++i) {
+    float x = 0.f;
+    cuda_check(cudaEventElapsedTime(&x, ev[2 * i], ev[2 * i + 1]), "elapsed");
+    ms[i] = x;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(s);
+  std::sort(ms.begin(), ms.end());
+  double sum = 0.0;
+  for (int i = trim; i < measure - trim; ++i) sum += ms[i];
+  return sum / static_cast<double>(measure - 2 * trim);
+}
+
+void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
+  if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_read_rows: table position " + std::to_string(t) + " out of range");
+  for (int64_t i = 0; i < n; ++i)
+    if (rows[i] < 0 || rows[i] >= specs_[t].hash_size)
+      fail(AS_INDEX, "table " + std::to_string(specs_[t].id) + ": row " + std::to_string(rows[i]) + " out of range");
+  if (n == 0) return;
+  DeviceGuard g(device_);
+  long long* drows = nullptr;
+  float* dst = nullptr;
+  cuda_check(cudaMalloc(&drows, sizeof(long long) * n), "malloc");
+  cuda_check(cudaMalloc(&dst, sizeof(float) * n * specs_[t].dim), "malloc");
+  cuda_check(cudaMemcpy(drows, rows, sizeof(long long) * n, cudaMemcpyHostToDevice), "rows H2D");
+  const long long w_off = htabs_[t].w_base + htabs_[t].row_off * specs_[t].dim;
+  gather_rows_kernel<<<grid_for(n * specs_[t].dim, 256), 256>>>(W_, w_off, specs_[t].dim, drows, n, dst);
+  cuda_check(cudaGetLastError(), "gather_rows_kernel");
+  cuda_check(cudaMemcpy(out, dst, sizeof(float) * n * specs_[t].dim, cudaMemcpyDeviceToHost), "rows D2H");
+  cudaFree(drows);
+  cudaFree(dst);
+}
+
+void EmbContext::read_momentum(int t, const int64_t* rows, int64_t n, float* out) {
+  if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_read_momentum: table position out of range");
+  if (n == 0) return;
+  DeviceGuard g(device_);
+  std::vector<float> all(static_cast<size_t>(specs_[t].hash_size));
+  cuda_check(cudaMemcpy(all.data(), M_ + htabs_[t].row_off, sizeof(float) * all.size(), cudaMemcpyDeviceToHost),
+             "momentum D2H");
+  for (int64_t i = 0; i < n; ++i) {
+    if (rows[i] < 0 || rows[i] >= specs_[t].hash_size) fail(AS_INDEX, "as_read_momentum: row out of range");
+    out[i] = all[static_cast<size_t>(rows[i])];
+  }
+}
+
+void EmbContext::read_buffer(int what, void* host, int64_t nbytes) {
+  DeviceGuard g(device_);
+  const void* src = nullptr;
+  int64_t want = 0;
+  switch (what) {
+    case 0: src = out_; want = B_ * sum_dim_ * 4; break;
+    case 1: src = bag_; want = L_ * 4; break;
+    case 2: src = skey_; want = L_ * 4; break;
+    case 3: src = sbag_; want = L_ * 4; break;
+    case 4: src = idx32_; want = L_ * 4; break;
+    default: fail(AS_CONFIG, "as_read_buffer: unknown buffer " + std::to_string(what));
+  }
+  if (what != 0) require_loaded("as_read_buffer");
+  if (nbytes != want)
+    fail(AS_SHAPE, "as_read_buffer: buffer " + std::to_string(what) + " has " + std::to_string(want) +
+                       " bytes, caller passed " + std::to_string(nbytes));
+  if (want) cuda_check(cudaMemcpy(host, src, static_cast<size_t>(want), cudaMemcpyDeviceToHost), "read D2H");
+}
+
+void EmbContext::write_table(int t, const float* w, const float* m) {
+  if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_write_table: table position out of range");
+  DeviceGuard g(device_);
+  const size_t rows = static_cast<size_t>(specs_[t].hash_size);
+  if (w) {
+    const long long w_off = htabs_[t].w_base + htabs_[t].row_off * specs_[t].dim;
+    cuda_check(cudaMemcpy(W_ + w_off, w, sizeof(float) * rows * specs_[t].dim, cudaMemcpyHostToDevice), "W H2D");
+  }
+  if (m) cuda_check(cudaMemcpy(M_ + htabs_[t].row_off, m, sizeof(float) * rows, cudaMemcpyHostToDevice), "M H2D");
+}
+
+void EmbContext::info(as_ctx_info* o) const {
+  std::memset(o, 0, sizeof *o);
+  o->device = device_;
+  o->n_tables = T_;
+  o->batch_size = B_;
+  o->sum_dim = sum_dim_;
+  o->total_rows = total_rows_;
+  o->n_lookups = loaded_ ? L_ : 0;
+  o->n_chunks = loaded_ ? n_chunks_ : 0;
+  o->device_bytes = bytes_;
+  o->pooled = out_;
+  o->weights = W_;
+  o->momentum = M_;
+  // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 5 + 1 + (end_bit_ + 7) / 8);
+}
+
+}  // namespace asb

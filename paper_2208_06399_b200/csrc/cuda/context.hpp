@@ -1,0 +1,87 @@
+// Device context: one shard of tables resident on one B200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../host/host.hpp"
+#include "types.hpp"
+
+namespace asb {
+
+void cuda_check(cudaError_t e, const char* what);
+
+class EmbContext {
+ public:
+  EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed);
+  ~EmbContext();
+  EmbContext(const EmbContext&) = delete;
+  EmbContext& operator=(const EmbContext&) = delete;
+
+  void load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
+            cudaStream_t s);
+  void forward(float* out, double* loss_dev, cudaStream_t s);
+  void backward(const float* grad, float lr, float eps, cudaStream_t s);
+  void step(float lr, float eps, double* loss_host, cudaStream_t s);
+  double measure(int warmup, int measure, int trim, bool flush, float lr, float eps);
+
+  void read_rows(int t, const int64_t* rows, int64_t n, float* out);
+  void read_momentum(int t, const int64_t* rows, int64_t n, float* out);
+  void read_buffer(int what, void* host, int64_t nbytes);
+  void write_table(int t, const float* w, const float* m);
+  void info(as_ctx_info* out) const;
+
+  int device() const { return device_; }
+  int n_tables() const { return T_; }
+  const as_table_spec& spec(int t) const { return specs_[t]; }
+
+ private:
+  void require_loaded(const char* what) const;
+  void ensure_capacity(int64_t L, int64_t n_chunks);
+  void* dalloc(size_t bytes);
+  SegParams seg_params(bool fwd) const;
+
+  int device_;
+  int T_;
+  int64_t B_;
+  uint64_t seed_;
+  std::vector<as_table_spec> specs_;
+  std::vector<DevTable> htabs_;
+  int64_t sum_dim_ = 0, total_rows_ = 0, total_w_ = 0;
+  int max_dim_ = 4;
+  int end_bit_ = 1;
+
+  DevTable* dtabs_ = nullptr;
+  float* W_ = nullptr;
+  float* M_ = nullptr;
+  float* out_ = nullptr;
+  int* off32_ = nullptr;
+  long long* stage_off_ = nullptr;
+  unsigned long long* err_ = nullptr;
+  double* loss_ = nullptr;
+  void* flush_ = nullptr;
+  size_t flush_bytes_ = 0;
+
+  // batch-dependent (grown on demand)
+  int64_t cap_L_ = 0, cap_chunks_ = 0;
+  int* idx32_ = nullptr;
+  int* bag_ = nullptr;
+  int* skey_ = nullptr;
+  int* sbag_ = nullptr;
+  long long* stage_idx_ = nullptr;
+  int* chunk_table_ = nullptr;
+  float* carry_ = nullptr;
+  void* cub_tmp_ = nullptr;
+  size_t cub_bytes_ = 0;
+
+  int64_t L_ = 0;
+  int64_t n_chunks_ = 0;
+  bool loaded_ = false;
+  int64_t bytes_ = 0;
+  std::vector<void*> allocs_;
+};
+
+}  // namespace asb

@@ -1,0 +1,283 @@
+"""GPU parity of the sm_100a hot path against the CPU oracle, through the C-ABI.
+
+Tolerances:
+* forward: BIT-EXACT. Initial weights live on the grid k*2^-12 (|k| <= 512), so
+  every partial sum of a bag below 2^12 in magnitude is exact in fp32 whatever
+  the summation order; the fp64 oracle must therefore match exactly.
+* backward / updated rows and momentum: |gpu - ref| <= 1e-5*|ref| + 1e-7
+  (north star: 1e-5 relative fp32), ref in fp64.
+* index handling (bag segmentation, sorted unique rows, counts): bit-exact.
+"""
+import numpy as np
+import pytest
+
+from helpers import bag_ids, fp_close, grad_grid, to_oracle_tables, weight_rows
+
+pytestmark = pytest.mark.gpu
+
+LR, EPS = 0.05, 1e-6
+
+
+def streams_of(wl, tables):
+    return [(wl.find(t.id).offsets, wl.find(t.id).indices) for t in tables]
+
+
+def run_bwd_check(oracle, shard, tables, streams, grad, seed, B):
+    for t, tab in enumerate(tables):
+        r = oracle.backward_adagrad_f64(to_oracle_tables([tab])[0], B, *streams[t], grad, shard.cols[t], LR, EPS,
+                                        wseed=seed)
+        if len(r["rows"]) == 0:
+            continue
+        w = shard.read_rows(t, r["rows"])
+        ok, worst = fp_close(w, r["w"])
+        assert ok, f"table {tab.id}: updated rows off by {worst:.3g}x tolerance"
+        m = shard.read_momentum(t, r["rows"])
+        ok, worst = fp_close(m, r["m"])
+        assert ok, f"table {tab.id}: momentum off by {worst:.3g}x tolerance"
+
+
+def test_cfg1_forward_bitexact_and_segmentation(P, oracle, cuda):
+    """BASELINE cfg 1: 10 tables, dim 64, batch 512, mean pooling 20."""
+    pool = P.generate_pool(0, 10, P.GeneratorConfig(dim_choices=(64,), pooling_mean_target=20.0))
+    B, seed = 512, 3
+    wl = P.generate_workload(0, pool, B)
+    st = streams_of(wl, pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(st)
+        sh.forward()
+        got = sh.read_pooled()
+        ref = oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed)
+        assert np.array_equal(got.astype(np.float64), ref)
+        # bag segmentation (bit-exact): K4 bag id per lookup, table-major
+        assert np.array_equal(sh.read_buffer(P.device.BAG_IDS), np.concatenate([bag_ids(o) for o, _ in st]))
+        # device index array = global rows
+        row_off = np.cumsum([0] + [t.hash_size for t in pool])[:-1]
+        glob = np.concatenate([i + r0 for (_, i), r0 in zip(st, row_off)]).astype(np.int32)
+        assert np.array_equal(sh.read_buffer(P.device.GLOBAL_ROWS), glob)
+        sh.backward(None, LR, EPS)
+        # stable sort by global row with bag ids: bit-exact
+        bags = np.concatenate([bag_ids(o) for o, _ in st])
+        order = np.argsort(glob, kind="stable")
+        assert np.array_equal(sh.read_buffer(P.device.SORTED_ROWS), glob[order])
+        assert np.array_equal(sh.read_buffer(P.device.SORTED_BAGS), bags[order])
+
+
+def test_cfg1_backward_rowwise_adagrad(P, oracle, cuda):
+    torch = cuda
+    pool = P.generate_pool(0, 10, P.GeneratorConfig(dim_choices=(64,), pooling_mean_target=20.0))
+    B, seed = 512, 5
+    wl = P.generate_workload(0, pool, B)
+    st = streams_of(wl, pool)
+    grad = grad_grid(11, B, 640)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(st)
+        sh.forward()
+        g = torch.from_numpy(grad).cuda()
+        sh.backward(g, LR, EPS)
+        torch.cuda.synchronize()
+        run_bwd_check(oracle, sh, pool, st, grad, seed, B)
+        # rows never looked up are untouched
+        t0 = pool[0]
+        touched = set(np.unique(st[0][1]).tolist())
+        probe = [r for r in range(0, t0.hash_size, max(1, t0.hash_size // 257)) if r not in touched][:64]
+        assert np.array_equal(sh.read_rows(0, probe), weight_rows(seed, t0.id, probe, t0.dim))
+
+
+@pytest.mark.parametrize("dims", [(4, 8, 12, 16, 20, 24, 32, 48), (64, 96, 128, 160, 192, 256), (384, 512, 1024)])
+def test_mixed_dims_one_launch(P, oracle, cuda, dims):
+    pool = P.generate_pool(1, len(dims), P.GeneratorConfig(hash_size_max=5e4, pooling_mean_target=30.0))
+    for t, d in zip(pool, dims):
+        t.dim = d
+    B, seed = 300, 9
+    wl = P.generate_workload(2, pool, B)
+    st = streams_of(wl, pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(st)
+        sh.forward()
+        pooled = sh.read_pooled()
+        ref = oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed)
+        assert np.array_equal(pooled.astype(np.float64), ref)
+        sh.backward(None, LR, EPS)
+        run_bwd_check(oracle, sh, pool, st, pooled, seed, B)
+
+
+def _handmade(B, lengths_per_table, rows_fn):
+    streams = []
+    for t, lens in enumerate(lengths_per_table):
+        off = np.zeros(B + 1, dtype=np.int64)
+        off[1:] = np.cumsum(lens)
+        idx = rows_fn(t, int(off[-1]))
+        streams.append((off, idx))
+    return streams
+
+
+@pytest.mark.parametrize("dim", [16, 128, 256])
+def test_long_bags_hot_rows_empty_tables(P, oracle, cuda, dim):
+    """Bags far longer than a chunk, a hot row spanning many chunks, runs of
+    empty bags, bags exactly one chunk long, and a table with no lookups."""
+    B = 64
+    rng = np.random.default_rng(0)
+    chunk = max(32, min(4096, (65536 // (dim * 4)) // 32 * 32))
+    lens = [
+        np.array([0, 20000, 1, 0, 0, chunk, chunk, 2 * chunk + 1] + [3] * (B - 8)),
+        np.array([chunk - 1, 1, chunk + 1] + [0] * (B - 4) + [5000]),
+        np.zeros(B, dtype=np.int64),
+        rng.integers(0, 50, size=B),
+    ]
+    hash_sizes = [5000, 70, 10, 1000]
+
+    def rows(t, n):
+        if t == 1:
+            return np.zeros(n, dtype=np.int64) + 3  # one hot row, every lookup
+        r = rng.integers(0, hash_sizes[t], size=n)
+        r[: n // 2] = 7  # hot row in the first half
+        return r.astype(np.int64)
+
+    st = _handmade(B, lens, rows)
+    tables = [P.TableDesc(id=10 + t, dim=dim, hash_size=h, pooling_mean=1.0) for t, h in enumerate(hash_sizes)]
+    seed = 4
+    with P.EmbeddingShard(tables, B, weight_seed=seed) as sh:
+        sh.load(st)
+        sh.forward()
+        pooled = sh.read_pooled()
+        ref = oracle.forward_f64(to_oracle_tables(tables), B, st, wseed=seed)
+        ok, worst = fp_close(pooled, ref, rtol=0, atol=0)
+        assert ok, f"forward not bit-exact ({worst})"
+        sh.backward(None, LR, EPS)
+        run_bwd_check(oracle, sh, tables, st, pooled, seed, B)
+
+
+def test_multistep_dense_against_oracle(P, oracle, cuda):
+    """Three fwd/bwd steps with grad = pooled (loss 1/2|pooled|^2), weights
+    evolving in place; oracle keeps dense fp32 tables updated from fp64 math."""
+    pool = P.generate_pool(5, 5, P.GeneratorConfig(dim_choices=(8, 32, 64), hash_size_max=3000,
+                                                  pooling_mean_target=25.0))
+    B, seed = 200, 13
+    wl = P.generate_workload(5, pool, B)
+    st = streams_of(wl, pool)
+    W = [weight_rows(seed, t.id, np.arange(t.hash_size), t.dim) for t in pool]
+    M = [np.zeros(t.hash_size, dtype=np.float32) for t in pool]
+    ot = to_oracle_tables(pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(st)
+        for step in range(3):
+            sh.forward()
+            pooled = sh.read_pooled()
+            ref = oracle.forward_f64(ot, B, st, dense=W)
+            ok, worst = fp_close(pooled, ref, rtol=1e-5, atol=1e-6)
+            assert ok, f"step {step}: forward off by {worst:.3g}x tolerance"
+            sh.backward(None, LR, EPS)
+            grad = ref.astype(np.float32)
+            for t in range(len(pool)):
+                oracle.backward_adagrad_f64(ot[t], B, *st[t], grad, sh.cols[t], LR, EPS, W=W[t], M=M[t])
+            for t, tab in enumerate(pool):
+                allrows = np.arange(tab.hash_size)
+                ok, worst = fp_close(sh.read_rows(t, allrows), W[t], rtol=1e-5, atol=1e-6)
+                assert ok, f"step {step} table {tab.id}: weights off by {worst:.3g}x"
+
+
+def test_step_loss(P, cuda):
+    pool = P.generate_pool(0, 4, P.GeneratorConfig(hash_size_max=1e4))
+    B = 1000
+    wl = P.generate_workload(0, pool, B)
+    with P.EmbeddingShard(pool, B, weight_seed=1) as sh:
+        sh.load(wl)
+        sh.forward()
+        pooled = sh.read_pooled().astype(np.float64)
+        loss = sh.step(LR, EPS, want_loss=True)
+        assert abs(loss - 0.5 * (pooled ** 2).sum()) <= 1e-5 * max(1.0, loss)
+
+
+def test_load_validation_errors(P, cuda):
+    tables = [P.TableDesc(id=3, dim=16, hash_size=10), P.TableDesc(id=8, dim=16, hash_size=20)]
+    B = 4
+    good = [(np.array([0, 1, 2, 3, 4]), np.array([1, 2, 3, 4])), (np.array([0, 0, 1, 1, 2]), np.array([5, 19]))]
+    with P.EmbeddingShard(tables, B) as sh:
+        sh.load(good)
+        with pytest.raises(P.OffsetError, match="table 8: offsets must start at 0, got 1"):
+            sh.load([good[0], (np.array([1, 1, 1, 1, 2]), np.array([5, 19]))])
+        with pytest.raises(P.OffsetError, match="table 3: offsets must be nondecreasing at entry 2"):
+            sh.load([(np.array([0, 2, 1, 3, 4]), np.array([1, 2, 3, 4])), good[1]])
+        with pytest.raises(P.OffsetError, match="table 8: final offset 2 != index count 3"):
+            sh.load([good[0], (np.array([0, 0, 1, 1, 2]), np.array([5, 19, 1]))])
+        with pytest.raises(P.IndexError_, match=r"table 8: index 20 out of range \[0, 20\)"):
+            sh.load([good[0], (np.array([0, 0, 1, 1, 2]), np.array([5, 20]))])
+        with pytest.raises(P.IndexError_, match=r"table 3: index -1 out of range"):
+            sh.load([(np.array([0, 1, 2, 3, 4]), np.array([1, -1, 3, 4])), good[1]])
+        with pytest.raises(P.StateError):
+            sh.forward()  # failed load leaves no batch loaded
+        sh.load(good)
+        sh.forward()
+
+
+def test_bad_dims_rejected(P, cuda):
+    with pytest.raises(P.ConfigError):
+        P.EmbeddingShard([P.TableDesc(id=0, dim=6, hash_size=10)], 4)
+    with pytest.raises(P.ConfigError):
+        P.EmbeddingShard([P.TableDesc(id=0, dim=2048, hash_size=10)], 4)
+
+
+def test_measure_protocol_and_measure_plan(P, cuda):
+    pool = P.generate_pool(0, 12, P.GeneratorConfig(hash_size_max=1e5))
+    B = 4096
+    wl = P.generate_workload(0, pool, B)
+    with P.EmbeddingShard(pool, B) as sh:
+        sh.load(wl)
+        ms = sh.measure(2, 5, 1, True)
+        assert ms > 0
+        with pytest.raises(P.ConfigError, match="need measure - 2\\*trim >= 1"):
+            sh.measure(1, 4, 2, True)
+    task = P.ShardingTask(pool, 3, [sum(t.size_bytes() for t in pool)] * 3)
+    plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
+    costs = P.measure_plan(plan, task, wl, P.BenchConfig(warmup=1, measure=3, trim=1))
+    assert len(costs) == 3 and all(c > 0 for c in costs)
+    # an empty shard reports its (small, positive) launch time, not 0
+    empty = P.ShardingPlan([0] * len(pool))
+    c2 = P.measure_plan(empty, task, wl, P.BenchConfig(warmup=1, measure=3, trim=1))
+    assert c2[1] >= 0 and c2[0] > c2[1]
+    other = P.generate_pool(1, 13)[12:]
+    with pytest.raises(P.LookupError_):
+        P.measure_plan(P.ShardingPlan([0]), P.ShardingTask(other, 1, [10 ** 12]), wl,
+                       P.BenchConfig(warmup=0, measure=1, trim=0))
+    with pytest.raises(P.ConfigError):
+        P.measure_plan(P.ShardingPlan([5] * len(pool)), task, wl)
+
+
+def test_cfg2_full_size_properties(P, cuda):
+    """BASELINE cfg 2 at full size (50 tables, dim 128, B=65536): size-independent
+    checks — column sums of the pooled output equal sum over unique rows of
+    count * W[row] (exact on the weight grid, checked per table in fp64) and
+    the momentum of sampled unique rows equals |g_r|^2/D."""
+    pool = P.generate_pool(0, 856)[:50]
+    for t in pool:
+        t.dim = 128
+    B, seed = 65536, 0
+    wl = P.generate_workload(0, pool, B)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(wl)
+        sh.forward()
+        pooled = sh.read_pooled()
+        rng = np.random.default_rng(0)
+        for t in rng.choice(len(pool), size=6, replace=False):
+            tab = pool[t]
+            idx = wl.find(tab.id).indices
+            rows, counts = np.unique(idx, return_counts=True)
+            W = weight_rows(seed, tab.id, rows, tab.dim).astype(np.float64)
+            want = (W * counts[:, None]).sum(0)
+            got = pooled[:, sh.cols[t]:sh.cols[t] + 128].astype(np.float64).sum(0)
+            assert np.allclose(got, want, rtol=1e-9, atol=1e-6)
+        sh.backward(None, LR, EPS)
+        for t in rng.choice(len(pool), size=3, replace=False):
+            tab = pool[t]
+            s = wl.find(tab.id)
+            bags = bag_ids(s.offsets)
+            rows, inv = np.unique(s.indices, return_inverse=True)
+            order = np.argsort(inv, kind="stable")
+            bounds = np.searchsorted(inv[order], np.arange(len(rows) + 1))
+            pick = rng.choice(len(rows), size=min(200, len(rows)), replace=False)
+            G = pooled[:, sh.cols[t]:sh.cols[t] + 128].astype(np.float64)
+            got = sh.read_momentum(int(t), rows[pick])
+            for q, k in enumerate(pick):
+                g = G[bags[order[bounds[k]:bounds[k + 1]]]].sum(0)
+                want = (g @ g) / 128
+                assert abs(got[q] - want) <= 1e-5 * want + 1e-30
