@@ -1,0 +1,492 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 embedding-bag hot path (AutoShard, arXiv 2208.06399).
+
+One "step" = one training pass of the multi-table pooled embedding bag over one
+batch: K4 bag expansion -> sum-pooled forward -> (N>1: all-to-all of pooled
+rows to the sample owners, loss 1/2|pooled|^2, all-to-all of the gradient back)
+-> radix sort of the lookups by row -> segment-sum + exact row-wise Adagrad in
+place. Metric: samples/s of the whole job (BASELINE.json).
+
+  python bench.py                       # N=1, BASELINE cfg 2 (50 tables, dim 128, B=65536)
+  torchrun --nproc-per-node N bench.py --gpus N   # cfg 4 (856 tables) sharded over N GPUs
+  python bench.py --impl reference      # CPU baseline arm (oracle port, all host cores)
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LR, EPS = 0.01, 1e-8
+WEIGHT_SEED = 0
+METRIC = "emb-bag fwd+bwd samples/s"
+
+
+# ---------------------------------------------------------------------------
+# workloads (all from the bit-exact reference generator)
+# ---------------------------------------------------------------------------
+def build_workload(P, name):
+    if name == "cfg2":
+        tables = P.generate_pool(0, 856)[:50]
+        for t in tables:
+            t.dim = 128
+        return tables, 65536, "cfg2: generate_pool(0,856)[0:50], dim:=128, batch 65536, zipf 1.05"
+    if name == "cfg3":
+        tables = P.generate_pool(0, 100, P.GeneratorConfig(dim_choices=(32, 64, 128, 256)))
+        return tables, 65536, "cfg3: generate_pool(0,100,dims {32,64,128,256}), batch 65536"
+    if name == "cfg4":
+        return P.generate_pool(0, 856), 65536, "cfg4: generate_pool(0,856) dims {16,32}, batch 65536"
+    if name == "cfg1":
+        tables = P.generate_pool(0, 10, P.GeneratorConfig(dim_choices=(64,), pooling_mean_target=20.0))
+        return tables, 512, "cfg1: generate_pool(0,10,dim 64,pooling 20), batch 512"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def nominal_bytes(tables, B, L, U):
+    """SURVEY.md §8d algorithmic bytes (s = 4): per-phase split that sums to FWD+BWD."""
+    s = 4
+    T = len(tables)
+    SD = sum(t.dim for t in tables)
+    LD = sum(l * t.dim for l, t in zip(L, tables))
+    UD = sum(u * t.dim for u, t in zip(U, tables))
+    Lt, Ut = sum(L), sum(U)
+    phases = {
+        "bag_expand": s * T * (B + 1),
+        "fwd_segreduce": s * (Lt + LD + B * SD),
+        "fwd_fixup": 0,
+        "radix_sort": s * (Lt + T * (B + 1)),
+        "bwd_segreduce_adagrad": s * LD + 2 * s * UD + 2 * s * Ut,
+        "bwd_fixup": 0,
+    }
+    fwd = s * (Lt + T * (B + 1) + LD + B * SD)
+    bwd = s * (Lt + T * (B + 1) + LD) + 2 * s * UD + 2 * s * Ut
+    return fwd, bwd, phases
+
+
+def stream_stats(wl, tables):
+    L, U = [], []
+    for t in tables:
+        idx = wl.find(t.id).indices
+        L.append(int(len(idx)))
+        U.append(int(np.count_nonzero(np.bincount(idx, minlength=1))) if len(idx) else 0)
+    return L, U
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel, workload):
+    """dram bytes/launch of `kernel` from the committed ncu --set full summary, if it matches."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        e = d.get(workload, {}).get(kernel)
+        return float(e["dram_bytes_per_launch"]) if e else None
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port; test infrastructure, only ever the checker/baseline)
+# ---------------------------------------------------------------------------
+class CpuSample:
+    """oracle/orc_cpu_step_f32 (the CPU port of the path) on a prefix of the
+    tables whose dense fp32 weights fit max_weight_bytes; times scale to the
+    full workload by gathered bytes (sum L_t * dim_t)."""
+
+    def __init__(self, tables, wl, B, max_weight_bytes=3 << 30, threads=0):
+        from oracle import Oracle
+
+        self.o = o = Oracle()
+        sub, wb = [], 0
+        for t in tables:
+            b = t.hash_size * t.dim * 4
+            if sub and wb + b > max_weight_bytes:
+                continue
+            sub.append(t)
+            wb += b
+            if wb > max_weight_bytes * 0.9:
+                break
+        self.W = np.empty(sum(t.hash_size * t.dim for t in sub), dtype=np.float32)
+        off = 0
+        for t in sub:
+            o.fill_weights(WEIGHT_SEED, t, self.W[off:off + t.hash_size * t.dim].reshape(t.hash_size, t.dim))
+            off += t.hash_size * t.dim
+        self.M = np.zeros(sum(t.hash_size for t in sub), dtype=np.float32)
+        self.out = np.empty((B, sum(t.dim for t in sub)), dtype=np.float32)
+        self.streams = [(wl.find(t.id).offsets, wl.find(t.id).indices) for t in sub]
+        self.dims = [t.dim for t in sub]
+        self.hashes = [t.hash_size for t in sub]
+        self.sub, self.tables, self.B, self.threads = sub, tables, B, threads
+        ld_full = sum(len(wl.find(t.id).indices) * t.dim for t in tables)
+        ld_sub = sum(len(s[1]) * t.dim for s, t in zip(self.streams, sub))
+        self.scale = ld_full / max(1, ld_sub)
+        self.cores = 1
+
+    def step(self):
+        t0 = time.perf_counter()
+        self.cores = self.o.cpu_step_f32(self.dims, self.hashes, self.B, self.streams, self.W, self.M, self.out,
+                                         LR, EPS, self.threads)
+        return time.perf_counter() - t0
+
+    def result(self, t_sample, n):
+        sub = self.sub
+        return {
+            "value": round(self.B / (t_sample * self.scale), 2),
+            "unit": "samples/s",
+            "cores": self.cores,
+            "kind": "port",
+            "sample": (f"oracle/orc_cpu_step_f32 (fp32 fwd + radix-sort bwd + row-wise Adagrad, OpenMP) on "
+                       f"{len(sub)}/{len(self.tables)} tables (ids {sub[0].id}..{sub[-1].id}), full batch {self.B}; "
+                       f"median of {n} steps = {t_sample * 1e3:.1f} ms, scaled x{self.scale:.2f} by gathered bytes"),
+            "host": cpu_host(),
+        }
+
+
+def cpu_sample(tables, wl, B, steps=3):
+    cs = CpuSample(tables, wl, B)
+    cs.step()  # warm-up
+    t = statistics.median([cs.step() for _ in range(steps)])
+    return cs.result(t, steps)
+
+
+def cpu_host():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="auto", help="cfg1|cfg2|cfg3|cfg4 (auto: cfg2 at N=1, cfg4 at N>1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.profile_only:
+        raise SystemExit("--warmup must be >= 3")
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wname = args.workload if args.workload != "auto" else ("cfg2" if world == 1 else "cfg4")
+
+    if args.impl == "reference":
+        return run_reference(args, world, rank, wname)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2208_06399_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    tables_all, B, wdesc = build_workload(P, wname)
+    if world > 1:
+        if B % world:
+            raise SystemExit("batch must divide by the GPU count")
+        budget = [int(180e9)] * world
+        task = P.ShardingTask(tables_all, world, budget)
+        plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
+        plan_name = "lookup-greedy (planners.hpp:73-107)"
+        mine = [t for t, k in zip(tables_all, plan.assignment) if k == rank]
+    else:
+        plan_name = "single shard"
+        mine = list(tables_all)
+
+    wl = P.generate_workload(0, mine, B)  # subset-stable: identical to the full-pool streams
+    wl.pin()
+    L, U = stream_stats(wl, mine)
+    shard = P.EmbeddingShard(mine, B, device=local, weight_seed=WEIGHT_SEED)
+    shard.load(wl)
+    stream = torch.cuda.current_stream()
+    SD = shard.sum_dim
+    pooled = shard.pooled_tensor()
+
+    # N>1 plumbing: pooled [B, SD_g] rows of peer p are contiguous -> all_to_all_single
+    if world > 1:
+        sds = [0] * world
+        sds[rank] = SD
+        t = torch.tensor(sds, device="cuda", dtype=torch.int64)
+        dist.all_reduce(t)
+        sds = t.tolist()
+        bl = B // world
+        recv = torch.empty(bl * sum(sds), device="cuda", dtype=torch.float32)
+        gback = torch.empty(B * SD, device="cuda", dtype=torch.float32)
+        in_split = [bl * SD] * world
+        out_split = [bl * s for s in sds]
+
+    def step():
+        shard.forward(pooled, stream=stream)
+        if world > 1:
+            dist.all_to_all_single(recv, pooled.view(-1), out_split, in_split)
+            # dense part out of scope: loss 1/2|pooled|^2 -> dL/dpooled = pooled (recv)
+            dist.all_to_all_single(gback, recv, in_split, out_split)
+            shard.backward(gback, LR, EPS, stream=stream)
+        else:
+            shard.backward(pooled, LR, EPS, stream=stream)
+
+    props = torch.cuda.get_device_properties(local)
+    l2 = getattr(props, "L2_cache_size", 126 << 20) or (126 << 20)
+    flush_buf = torch.empty(2 * l2 // 4 + 1024, device="cuda", dtype=torch.float32)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed between steps (flush not timed) ----
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    shard.profile_read(reset=True)
+    sampler = ClockSampler(local) if not args.profile_only else None
+    if sampler:
+        sampler.__enter__()
+    barrier()
+    for i in range(K):
+        flush_buf.fill_(float(i))
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    barrier()
+    if sampler:
+        sampler.__exit__()
+    _, launches = shard.profile_read(reset=True)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = sum(step_ms)
+    tt = torch.tensor([t_local], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max = float(tt.item())  # ms over K steps, max over ranks
+    ms_per_step = t_max / K
+    value = B * K / (t_max / 1e3)
+
+    # ---- per-kernel timing pass (events between phases), same stream ----
+    shard.profile(True)
+    for i in range(K):
+        flush_buf.fill_(float(i))
+        step()
+    torch.cuda.synchronize()
+    phase_ms, _ = shard.profile_read(reset=True)
+    shard.profile(False)
+    fwd_b, bwd_b, phase_bytes = nominal_bytes(mine, B, L, U)
+    peak, peak_kind = measured_peak_hbm()
+    dom = max(phase_ms, key=phase_ms.get)
+    dom_ms = phase_ms[dom] / K
+    achieved = phase_bytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    traffic = ncu_traffic(dom, wname) if world == 1 else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "algorithmic_bytes_per_launch": phase_bytes[dom],
+                "ms_per_launch": round(dom_ms, 4)}
+    step_gbs = (fwd_b + bwd_b) / (ms_per_step / 1e3) / 1e9
+
+    # ---- e2e through the public API: pinned host int64 streams -> device each step ----
+    e2e = None
+    if not args.no_e2e and not args.profile_only:
+        h2d = sum(8 * (B + 1) + 8 * l for l in L) + 40 * len(mine)
+        d2h = 8 + 8
+        for _ in range(2):
+            shard.load(wl, stream=stream)
+            shard.step(LR, EPS, want_loss=True, stream=stream)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(K):
+            shard.load(wl, stream=stream)  # H2D of this step's inputs + on-device validation
+            if world > 1:
+                step()
+                loss = torch.dot(recv, recv).mul_(0.5).item()  # step result to host
+            else:
+                loss = shard.step(LR, EPS, want_loss=True, stream=stream)  # D2H of the loss
+        barrier()
+        te = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(B * K / float(te.item()), 1), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": d2h, "ms_per_step": round(float(te.item()) * 1e3 / K, 3),
+               "loss_last": loss}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile_only:
+        cpu = cpu_sample(mine, wl, B)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 1),
+            "unit": "samples/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None,
+            "dtype": "fp32",
+            "data": "synthetic (reference generator, bit-exact; weights: counter-hash grid init)",
+            "config": {
+                "workload": wname,
+                "desc": wdesc,
+                "tables": len(tables_all),
+                "global_batch": B,
+                "sum_dim": sum(t.dim for t in tables_all),
+                "lookups": int(sum(L)) if world == 1 else None,
+                "plan": plan_name,
+                "parallelism": "table-wise" if world > 1 else "single",
+                "step": "K4 bag-expand + fwd segreduce + fixup + radix sort + bwd segreduce/row-wise Adagrad + fixup"
+                        + (" + 2x NCCL all_to_all" if world > 1 else "") + "; grad = pooled (loss 1/2|pooled|^2)",
+                "l2": "flushed (2x L2 fill) between timed steps, flush excluded from step time",
+                "lr": LR,
+                "eps": EPS,
+            },
+            "roofline": roofline,
+            "step_roofline": {"bytes_fwd": fwd_b, "bytes_bwd": bwd_b, "achieved_gbs": round(step_gbs, 1),
+                              "frac": round(step_gbs / peak, 4)},
+            "phase_ms_per_step": {k: round(v / K, 4) for k, v in phase_ms.items()},
+            "gpu_launches": int(launches),
+            "launches_per_step": launches / K,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": sampler.summary() if sampler else None,
+            "step_ms_min_median_max": [round(min(step_ms), 4), round(statistics.median(step_ms), 4),
+                                       round(max(step_ms), 4)],
+        }
+        print(json.dumps(line), flush=True)
+    shard.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank, wname):
+    """CPU arm: the reference has no embedding arithmetic, so the
+    reference-side implementation of the path is the oracle port (fp32, OpenMP,
+    all host threads), timed on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import paper_2208_06399_b200 as P  # host generator only (no device calls)
+
+    tables, B, wdesc = build_workload(P, wname)
+    wl = P.generate_workload(0, tables, B)
+    cs = CpuSample(tables, wl, B)
+    for _ in range(args.warmup):
+        cs.step()
+    ts = [cs.step() for _ in range(args.steps)]
+    cpu = cs.result(statistics.median(ts), len(ts))
+    v = cpu["value"]
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(v, 2),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(B / v * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic (reference generator, bit-exact)",
+        "config": {"workload": wname, "desc": wdesc, "tables": len(tables), "global_batch": B},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(v, 2), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

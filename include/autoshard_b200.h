@@ -230,6 +230,16 @@ typedef struct as_ctx_info {
 } as_ctx_info;
 AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info);
 
+/* Per-kernel CUDA-event timing for roofline accounting (bench.py). When
+ * enabled, every phase of as_forward / as_backward_rowwise_adagrad records an
+ * event pair on the launching stream. as_profile_read synchronises and returns
+ * the accumulated ms per phase: [0] bag_expand (K4), [1] forward segment
+ * reduce (K1), [2] forward fixup, [3] radix sort (K2), [4] backward segment
+ * reduce + Adagrad (K3), [5] backward fixup; *launches = kernels launched. */
+#define AS_NUM_PHASES 6
+AS_API as_status as_profile_enable(as_ctx* ctx, int32_t enable);
+AS_API as_status as_profile_read(as_ctx* ctx, double* ms_per_phase, int64_t* launches, int32_t reset);
+
 /* Readbacks for parity (synchronise). */
 /* rows: n row ids (table-local) of ctx table position t -> out [n, dim] fp32. */
 AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out);

@@ -109,6 +109,7 @@ class Oracle:
         L.orc_degree_of_balance.argtypes = [C.POINTER(C.c_double), C.c_int]
         L.orc_weight_init.restype = C.c_float
         L.orc_weight_init.argtypes = [C.c_uint64, C.c_int32, C.c_int64, C.c_int32]
+        L.orc_fill_weights.argtypes = [C.c_uint64, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_float)]
         L.orc_grad_init.restype = C.c_float
         L.orc_grad_init.argtypes = [C.c_uint64, C.c_int64, C.c_int64]
         L.orc_emb_forward_f64.argtypes = [C.c_int, C.POINTER(TableC), C.c_int64,
@@ -198,6 +199,13 @@ class Oracle:
             for d in range(table.dim):
                 W[r, d] = f(seed, table.id, r, d)
         return W
+
+    def fill_weights(self, seed, table, out=None):
+        """Dense [hash, dim] fp32 init of one table (OpenMP C)."""
+        if out is None:
+            out = np.empty((table.hash_size, table.dim), dtype=np.float32)
+        self.lib.orc_fill_weights(seed, table.id, table.hash_size, table.dim, _p(out, C.c_float))
+        return out
 
     def grad_init(self, seed, B, ncols):
         f = self.lib.orc_grad_init

@@ -386,6 +386,12 @@ float orc_grad_init(uint64_t seed, int64_t b, int64_t col) {
   return (float)k * 0x1.0p-12f;
 }
 
+void orc_fill_weights(uint64_t seed, int32_t table_id, int64_t rows, int32_t dim, float* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < rows; ++r)
+    for (int32_t d = 0; d < dim; ++d) out[r * dim + d] = orc_weight_init(seed, table_id, r, d);
+}
+
 void orc_emb_forward_f64(int T, const orc_table* tabs, int64_t B, const int64_t* const* offsets,
                          const int64_t* const* indices, const float* const* W, uint64_t wseed,
                          double* out) {

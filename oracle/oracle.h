@@ -81,6 +81,8 @@ double orc_degree_of_balance(const double* c, int n);
  * k * 2^-12, k in [-512, 511]. Same definition as the device init kernel
  * (DESIGN.md "weight init"). */
 float orc_weight_init(uint64_t seed, int32_t table_id, int64_t row, int32_t d);
+/* Dense init of a whole table (OpenMP), out [rows, dim]. */
+void orc_fill_weights(uint64_t seed, int32_t table_id, int64_t rows, int32_t dim, float* out);
 /* Synthetic gradient G[b, col]: same grid, independent stream. */
 float orc_grad_init(uint64_t seed, int64_t b, int64_t col);
 

@@ -112,6 +112,8 @@ SIGNATURES = {
     "as_measure": (i32, [vp, i32, i32, i32, i32, f32, f32, P(f64)]),
     "as_measure_plan": (i32, [T_SPEC, i32, i32, P(i32), vp, P(i32), i32, P(BenchConfigC), P(f64)]),
     "as_ctx_info_get": (i32, [vp, P(CtxInfoC)]),
+    "as_profile_enable": (i32, [vp, i32]),
+    "as_profile_read": (i32, [vp, P(f64), P(i64), i32]),
     "as_read_rows": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_momentum": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_buffer": (i32, [vp, i32, vp, i64]),

@@ -398,6 +398,21 @@ AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info) {
   });
 }
 
+AS_API as_status as_profile_enable(as_ctx* ctx, int32_t enable) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->impl->profile_enable(enable != 0);
+  });
+}
+
+AS_API as_status as_profile_read(as_ctx* ctx, double* ms, int64_t* launches, int32_t reset) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(ms, "ms");
+    ctx->impl->profile_read(ms, launches, reset != 0);
+  });
+}
+
 AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out) {
   return guard([&] {
     need(ctx, "ctx");

@@ -92,6 +92,60 @@ unsigned grid_for(long long work, long long per_block) {
 
 }  // namespace
 
+cudaEvent_t EmbContext::ev_get() {
+  if (ev_pool_.empty()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "event");
+    return e;
+  }
+  cudaEvent_t e = ev_pool_.back();
+  ev_pool_.pop_back();
+  return e;
+}
+
+// Records a CUDA event pair around one phase when profiling is on.
+struct EmbContext::Phase {
+  EmbContext* c;
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  Phase(EmbContext* ctx, int phase, cudaStream_t st) : c(ctx), id(phase), s(st) {
+    if (c->prof_) {
+      a = c->ev_get();
+      cuda_check(cudaEventRecord(a, s), "event");
+    }
+  }
+  ~Phase() {
+    if (a) {
+      cudaEvent_t b = c->ev_get();
+      cudaEventRecord(b, s);
+      c->ev_used_.push_back({id, {a, b}});
+    }
+  }
+};
+
+void EmbContext::profile_enable(bool on) { prof_ = on; }
+
+void EmbContext::profile_read(double* ms, int64_t* launches, bool reset) {
+  DeviceGuard g(device_);
+  for (int i = 0; i < kPhases; ++i) ms[i] = 0.0;
+  for (auto& u : ev_used_) {
+    cuda_check(cudaEventSynchronize(u.second.second), "event sync");
+    float x = 0.f;
+    cuda_check(cudaEventElapsedTime(&x, u.second.first, u.second.second), "elapsed");
+    ms[u.first] += x;
+  }
+  if (launches) *launches = launches_;
+  if (reset) {
+    for (auto& u : ev_used_) {
+      ev_pool_.push_back(u.second.first);
+      ev_pool_.push_back(u.second.second);
+    }
+    ev_used_.clear();
+    launches_ = 0;
+  }
+}
+
 void* EmbContext::dalloc(size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 16;
@@ -175,6 +229,11 @@ EmbContext::~EmbContext() {
   cudaSetDevice(device_);
   cudaDeviceSynchronize();
   for (void* p : allocs_) cudaFree(p);
+  for (auto& u : ev_used_) {
+    cudaEventDestroy(u.second.first);
+    cudaEventDestroy(u.second.second);
+  }
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -310,9 +369,13 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   if (T_ == 0) return;
   float* target = out ? out : out_;
   const long long nb = (long long)T_ * B_;
-  bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
-                                                                          target, sum_dim_);
-  cuda_check(cudaGetLastError(), "bag_expand_kernel");
+  {
+    Phase ph(this, 0, s);
+    bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
+                                                                            target, sum_dim_);
+    cuda_check(cudaGetLastError(), "bag_expand_kernel");
+    ++launches_;
+  }
   if (n_chunks_ == 0) return;
   SegParams p = seg_params(true);
   p.W_ro = W_;
@@ -320,10 +383,17 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.out_stride = sum_dim_;
   p.loss = loss_dev;
   const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
-  seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
-  cuda_check(cudaGetLastError(), "seg_reduce_kernel<fwd>");
-  seg_fixup_kernel<true><<<grid, kBlock, 0, s>>>(p);
-  cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
+  {
+    Phase ph(this, 1, s);
+    seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
+    cuda_check(cudaGetLastError(), "seg_reduce_kernel<fwd>");
+  }
+  {
+    Phase ph(this, 2, s);
+    seg_fixup_kernel<true><<<grid, kBlock, 0, s>>>(p);
+    cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
+  }
+  launches_ += 2;
 }
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
@@ -331,10 +401,15 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   DeviceGuard g(device_);
   if (T_ == 0 || n_chunks_ == 0) return;
   size_t tmp = cub_bytes_;
+  {
+  Phase ph(this, 3, s);
   cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_),
                                              reinterpret_cast<unsigned*>(skey_), bag_, sbag_, (int)L_, 0,
                                              end_bit_, s),
              "cub SortPairs");
+  // onesweep: histogram + exclusive-sum + one pass per 8 key bits
+  launches_ += 2 + (end_bit_ + 7) / 8;
+  }
   SegParams p = seg_params(false);
   p.grad = grad ? grad : out_;
   p.grad_stride = sum_dim_;
@@ -343,10 +418,17 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   p.lr = lr;
   p.eps = eps;
   const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
-  seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
-  cuda_check(cudaGetLastError(), "seg_reduce_kernel<bwd>");
-  seg_fixup_kernel<false><<<grid, kBlock, 0, s>>>(p);
-  cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
+  {
+    Phase ph(this, 4, s);
+    seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
+    cuda_check(cudaGetLastError(), "seg_reduce_kernel<bwd>");
+  }
+  {
+    Phase ph(this, 5, s);
+    seg_fixup_kernel<false><<<grid, kBlock, 0, s>>>(p);
+    cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
+  }
+  launches_ += 2;
 }
 
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
@@ -470,7 +552,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 5 + 1 + (end_bit_ + 7) / 8);
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 5 + 2 + (end_bit_ + 7) / 8);
 }
 
 }  // namespace asb

@@ -34,6 +34,12 @@ class EmbContext {
   void write_table(int t, const float* w, const float* m);
   void info(as_ctx_info* out) const;
 
+  // Per-phase CUDA-event timing (bag_expand, fwd_seg, fwd_fixup, sort,
+  // bwd_seg, bwd_fixup) and launch counting, for bench.py's roofline.
+  static constexpr int kPhases = 6;
+  void profile_enable(bool on);
+  void profile_read(double* ms, int64_t* launches, bool reset);
+
   int device() const { return device_; }
   int n_tables() const { return T_; }
   const as_table_spec& spec(int t) const { return specs_[t]; }
@@ -81,6 +87,12 @@ class EmbContext {
   int64_t n_chunks_ = 0;
   bool loaded_ = false;
   int64_t bytes_ = 0;
+  int64_t launches_ = 0;
+  bool prof_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used_;
+  cudaEvent_t ev_get();
+  struct Phase;
   std::vector<void*> allocs_;
 };
 

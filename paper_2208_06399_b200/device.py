@@ -123,6 +123,19 @@ class EmbeddingShard:
         check(lib().as_measure(self._h, warmup, measure, trim, int(flush_l2), lr, eps, C.byref(ms)))
         return ms.value
 
+    # -- profiling ---------------------------------------------------------
+    PHASES = ("bag_expand", "fwd_segreduce", "fwd_fixup", "radix_sort", "bwd_segreduce_adagrad", "bwd_fixup")
+
+    def profile(self, enable: bool = True) -> None:
+        check(lib().as_profile_enable(self._h, int(enable)))
+
+    def profile_read(self, reset: bool = True):
+        """-> ({phase: ms accumulated}, kernel launches) since the last reset."""
+        ms = (C.c_double * len(self.PHASES))()
+        n = C.c_int64()
+        check(lib().as_profile_read(self._h, ms, C.byref(n), int(reset)))
+        return dict(zip(self.PHASES, list(ms))), n.value
+
     # -- introspection / readback -------------------------------------------
     def info(self) -> CtxInfoC:
         i = CtxInfoC()
