@@ -203,6 +203,10 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   stage_off_ = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
+  counters_ = static_cast<int*>(dalloc(sizeof(int) * 2));
+  int sms = 148;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
+  fixup_grid_ = static_cast<unsigned>(sms * 2);
   int l2 = 0;
   cuda_check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_), "L2 size");
   flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
@@ -237,7 +241,7 @@ EmbContext::~EmbContext() {
   if (prev >= 0) cudaSetDevice(prev);
 }
 
-void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks) {
+void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   auto drop = [this](void* p) {
     if (!p) return;
     auto it = std::find(allocs_.begin(), allocs_.end(), p);
@@ -263,12 +267,19 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks) {
   }
   if (n_chunks > cap_chunks_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
-    drop(chunk_table_);
     drop(carry_);
+    drop(completers_);
     const int64_t cap = std::max<int64_t>(n_chunks + n_chunks / 8, 64);
-    chunk_table_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     carry_ = static_cast<float*>(dalloc(sizeof(float) * cap * 2 * max_dim_));
+    completers_ = static_cast<int2*>(dalloc(sizeof(int2) * cap));
     cap_chunks_ = cap;
+  }
+  if (n_units > cap_units_) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    drop(unit_table_);
+    const int64_t cap = std::max<int64_t>(n_units + n_units / 8, 64);
+    unit_table_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    cap_units_ = cap;
   }
 }
 
@@ -276,24 +287,28 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
                       cudaStream_t s) {
   DeviceGuard g(device_);
   loaded_ = false;
-  int64_t L = 0, nch = 0;
+  int64_t L = 0, nch = 0, nun = 0;
   for (int t = 0; t < T_; ++t) {
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
     DevTable& d = htabs_[t];
+    const int R = 32 >> std::min(d.kind, 5);
+    const int64_t chunks = (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
+    const int64_t units = (chunks + R - 1) / R;
     d.idx_off = L;
     d.n_lookups = n_idx[t];
     d.chunk_off = static_cast<int>(nch);
+    d.unit_off = static_cast<int>(nun);
+    d.n_units = static_cast<int>(units);
     L += n_idx[t];
-    nch += (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
+    nch += units * R;
+    nun += units;
   }
   if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
   if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
-  ensure_capacity(L, nch);
-  std::vector<int> ctab(static_cast<size_t>(nch));
-  for (int t = 0; t < T_; ++t) {
-    const int64_t n = (htabs_[t].n_lookups + htabs_[t].chunk_len - 1) / htabs_[t].chunk_len;
-    std::fill(ctab.begin() + htabs_[t].chunk_off, ctab.begin() + htabs_[t].chunk_off + n, t);
-  }
+  ensure_capacity(L, nch, nun);
+  std::vector<int> utab(static_cast<size_t>(nun));
+  for (int t = 0; t < T_; ++t)
+    std::fill(utab.begin() + htabs_[t].unit_off, utab.begin() + htabs_[t].unit_off + htabs_[t].n_units, t);
   // H2D: raw int64 CSR into staging (pinned sources run at full PCIe rate).
   for (int t = 0; t < T_; ++t) {
     cuda_check(cudaMemcpyAsync(stage_off_ + (int64_t)t * (B_ + 1), offsets[t], sizeof(int64_t) * (B_ + 1),
@@ -307,9 +322,9 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
   if (T_ > 0)
     cuda_check(cudaMemcpyAsync(dtabs_, htabs_.data(), sizeof(DevTable) * T_, cudaMemcpyHostToDevice, s),
                "tables H2D");
-  if (nch > 0)
-    cuda_check(cudaMemcpyAsync(chunk_table_, ctab.data(), sizeof(int) * nch, cudaMemcpyHostToDevice, s),
-               "chunk table H2D");
+  if (nun > 0)
+    cuda_check(cudaMemcpyAsync(unit_table_, utab.data(), sizeof(int) * nun, cudaMemcpyHostToDevice, s),
+               "unit table H2D");
   cuda_check(cudaMemsetAsync(err_, 0xff, sizeof(unsigned long long), s), "err reset");
   if (T_ > 0) {
     const long long n = (long long)T_ * (B_ + 1);
@@ -317,9 +332,9 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
         stage_off_, T_, (int)B_, dtabs_, off32_, err_);
     cuda_check(cudaGetLastError(), "pack_offsets_kernel");
   }
-  if (nch > 0) {
-    pack_indices_kernel<<<grid_for(nch, kWarpsPerBlock), kBlock, 0, s>>>(stage_idx_, dtabs_, chunk_table_,
-                                                                        (int)nch, idx32_, err_);
+  if (nun > 0) {
+    pack_indices_kernel<<<grid_for(nun, kWarpsPerBlock), kBlock, 0, s>>>(stage_idx_, dtabs_, unit_table_,
+                                                                        (int)nun, idx32_, err_);
     cuda_check(cudaGetLastError(), "pack_indices_kernel");
   }
   unsigned long long err = 0;
@@ -343,6 +358,7 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
   }
   L_ = L;
   n_chunks_ = nch;
+  n_units_ = nun;
   loaded_ = true;
 }
 
@@ -354,8 +370,10 @@ SegParams EmbContext::seg_params(bool fwd) const {
   SegParams p;
   std::memset(&p, 0, sizeof p);
   p.tabs = dtabs_;
-  p.chunk_table = chunk_table_;
-  p.n_chunks = static_cast<int>(n_chunks_);
+  p.unit_table = unit_table_;
+  p.n_units = static_cast<int>(n_units_);
+  p.completers = completers_;
+  p.n_completers = counters_ + (fwd ? 0 : 1);
   p.seg = fwd ? bag_ : skey_;
   p.src = fwd ? idx32_ : sbag_;
   p.carry = carry_;
@@ -382,7 +400,8 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.out = target;
   p.out_stride = sum_dim_;
   p.loss = loss_dev;
-  const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
+  const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
+  cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int), s), "counter reset");
   {
     Phase ph(this, 1, s);
     seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
@@ -390,7 +409,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   }
   {
     Phase ph(this, 2, s);
-    seg_fixup_kernel<true><<<grid, kBlock, 0, s>>>(p);
+    seg_fixup_kernel<true><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
   }
   launches_ += 2;
@@ -417,7 +436,8 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   p.M = M_;
   p.lr = lr;
   p.eps = eps;
-  const unsigned grid = grid_for(n_chunks_, kWarpsPerBlock);
+  const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
+  cuda_check(cudaMemsetAsync(counters_ + 1, 0, sizeof(int), s), "counter reset");
   {
     Phase ph(this, 4, s);
     seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
@@ -425,7 +445,7 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   }
   {
     Phase ph(this, 5, s);
-    seg_fixup_kernel<false><<<grid, kBlock, 0, s>>>(p);
+    seg_fixup_kernel<false><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
   }
   launches_ += 2;

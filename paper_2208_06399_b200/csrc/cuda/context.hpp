@@ -46,7 +46,7 @@ class EmbContext {
 
  private:
   void require_loaded(const char* what) const;
-  void ensure_capacity(int64_t L, int64_t n_chunks);
+  void ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units);
   void* dalloc(size_t bytes);
   SegParams seg_params(bool fwd) const;
 
@@ -78,7 +78,12 @@ class EmbContext {
   int* skey_ = nullptr;
   int* sbag_ = nullptr;
   long long* stage_idx_ = nullptr;
-  int* chunk_table_ = nullptr;
+  int* unit_table_ = nullptr;
+  int2* completers_ = nullptr;
+  int* counters_ = nullptr;  // [0] fwd completers, [1] bwd completers
+  unsigned fixup_grid_ = 296;
+  int64_t cap_units_ = 0;
+  int64_t n_units_ = 0;
   float* carry_ = nullptr;
   void* cub_tmp_ = nullptr;
   size_t cub_bytes_ = 0;

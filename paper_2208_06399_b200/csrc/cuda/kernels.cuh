@@ -40,31 +40,35 @@ __device__ __forceinline__ void st4_streaming(float* p, float4 v) {
   __stcs(reinterpret_cast<float4*>(p), v);
 }
 
-// Group (GL lanes) sum, every lane of the warp participates.
 template <int GL>
-__device__ __forceinline__ float group_sum(float x) {
+__device__ __forceinline__ unsigned low_bits() {
+  return GL >= 32 ? 0xffffffffu : ((1u << GL) - 1u);
+}
+
+// Sum over the GL lanes of a group; `mask` = the group's lanes (all of them
+// must be active, the caller's branch is group-uniform).
+template <int GL>
+__device__ __forceinline__ float group_sum(float x, unsigned mask) {
 #pragma unroll
-  for (int m = GL / 2; m >= 1; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+  for (int m = GL / 2; m >= 1; m >>= 1) x += __shfl_xor_sync(mask, x, m);
   return x;
 }
 
-// Segment epilogue, executed by the GL lanes of one group (predicated by
-// `active`, all lanes call it so the group reduction stays converged).
+// Segment epilogue, executed by the GL lanes of one group.
+//   forward : pooled[bag, col_t + :] = v            (+ loss 1/2|v|^2)
+//   backward: m_r += |g|^2/D; W_r -= lr * g / (sqrt(m_r) + eps)   (FBGEMM exact row-wise Adagrad)
 template <bool FWD, int GL, int NV>
-__device__ __forceinline__ void finish_segment(const SegParams& p, const DevTable& tb, bool active,
-                                               int seg, const float4 (&v)[NV], int c,
-                                               float& loss_acc) {
+__device__ __forceinline__ void finish_segment(const SegParams& p, const DevTable& tb, unsigned gmask, int seg,
+                                               const float4 (&v)[NV], int c, float& loss_acc) {
   const int nvec = tb.dim >> 2;
   if constexpr (FWD) {
-    if (active) {
-      float* o = p.out + (long long)seg * p.out_stride + tb.col;
+    float* o = p.out + (long long)seg * p.out_stride + tb.col;
 #pragma unroll
-      for (int w = 0; w < NV; ++w) {
-        const int cv = c + w * GL;
-        if (cv < nvec) {
-          st4_streaming(o + cv * 4, v[w]);
-          loss_acc += f4dot(v[w]);
-        }
+    for (int w = 0; w < NV; ++w) {
+      const int cv = c + w * GL;
+      if (cv < nvec) {
+        st4_streaming(o + cv * 4, v[w]);
+        loss_acc += f4dot(v[w]);
       }
     }
   } else {
@@ -72,33 +76,30 @@ __device__ __forceinline__ void finish_segment(const SegParams& p, const DevTabl
 #pragma unroll
     for (int w = 0; w < NV; ++w)
       if (c + w * GL < nvec) sq += f4dot(v[w]);
-    sq = group_sum<GL>(sq);
-    if (active) {
-      // exact row-wise Adagrad (FBGEMM semantics): m += |g|^2/D; W -= lr*g/(sqrt(m)+eps)
-      const float m = p.M[seg] + sq / (float)tb.dim;
-      const float mult = p.lr / (sqrtf(m) + p.eps);
-      float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
+    sq = group_sum<GL>(sq, gmask);
+    const float m = p.M[seg] + sq / (float)tb.dim;
+    const float mult = p.lr / (sqrtf(m) + p.eps);
+    float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
 #pragma unroll
-      for (int w = 0; w < NV; ++w) {
-        const int cv = c + w * GL;
-        if (cv < nvec) {
-          float4* q = reinterpret_cast<float4*>(wr + cv * 4);
-          float4 x = *q;
-          x.x -= mult * v[w].x;
-          x.y -= mult * v[w].y;
-          x.z -= mult * v[w].z;
-          x.w -= mult * v[w].w;
-          *q = x;
-        }
+    for (int w = 0; w < NV; ++w) {
+      const int cv = c + w * GL;
+      if (cv < nvec) {
+        float4* q = reinterpret_cast<float4*>(wr + cv * 4);
+        float4 x = *q;
+        x.x -= mult * v[w].x;
+        x.y -= mult * v[w].y;
+        x.z -= mult * v[w].z;
+        x.w -= mult * v[w].w;
+        *q = x;
       }
-      if (c == 0) p.M[seg] = m;
     }
+    if (c == 0) p.M[seg] = m;
   }
 }
 
-template <int NV>
-__device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int which, int nvec, int GL,
-                                            int c, const float4 (&v)[NV]) {
+template <int GL, int NV>
+__device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int which, int nvec, int c,
+                                            const float4 (&v)[NV]) {
   float* dst = p.carry + ((long long)chunk * 2 + which) * p.carry_stride;
 #pragma unroll
   for (int w = 0; w < NV; ++w) {
@@ -107,22 +108,30 @@ __device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int w
   }
 }
 
-// One warp reduces one chunk of one table.
+// One warp = one "unit" = 32/GL consecutive chunks of one table; each group
+// of GL lanes walks its own chunk sequentially: gather a row, add it to the
+// running sum, finish the segment when the key changes. Per element a lane
+// issues one shuffle (row id), one 16-byte gather per float4 column and the
+// adds; the segment-end test is a bit of a group mask built with ballots.
 template <bool FWD, int GL, int NV>
-__device__ __forceinline__ void seg_chunk(const SegParams& p, const DevTable& tb, int chunk) {
-  constexpr int R = 32 / GL;   // elements per round
-  constexpr int RS = GL;       // rounds per 32-element super-round
-  constexpr int U = (RS < 8 / NV ? RS : (8 / NV > 0 ? 8 / NV : 1));  // rounds per load batch
+__device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit) {
+  constexpr int R = 32 / GL;                     // chunks (groups) per warp
+  constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
+  constexpr int Q = SR / GL;                     // elements held per lane per super-round
+  constexpr int U = NV >= 8 ? 1 : 8 / NV;        // gathers in flight per lane
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
   const int c = lane % GL;
+  const unsigned gmask = low_bits<GL>() << (g * GL);
   const int nvec = tb.dim >> 2;
+  const int C = tb.chunk_len;
+  const int lchunk = (unit - tb.unit_off) * R + g;
+  const int chunk = tb.chunk_off + lchunk;
   const long long t_lo = tb.idx_off, t_hi = tb.idx_off + tb.n_lookups;
-  const long long j_lo = t_lo + (long long)(chunk - tb.chunk_off) * tb.chunk_len;
-  const long long j_hi = min(j_lo + (long long)tb.chunk_len, t_hi);
-  if (j_lo >= j_hi) return;
-  const int prev_seg = j_lo > t_lo ? __ldg(p.seg + j_lo - 1) : -1;
-  const int next_seg = j_hi < t_hi ? __ldg(p.seg + j_hi) : -2;
+  const long long j_lo = t_lo + (long long)lchunk * C;
+  const long long j_hi = min(j_lo + (long long)C, t_hi);
+  const bool live = j_lo < j_hi;
+  const int prev_seg = (live && j_lo > t_lo) ? __ldg(p.seg + j_lo - 1) : -1;
 
   const float* gbase;
   long long gstride;
@@ -134,31 +143,40 @@ __device__ __forceinline__ void seg_chunk(const SegParams& p, const DevTable& tb
     gstride = p.grad_stride;
   }
 
-  float4 carry[NV];
+  float4 acc[NV];
 #pragma unroll
-  for (int w = 0; w < NV; ++w) carry[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-  int carry_seg = -3;
+  for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
   float loss_acc = 0.f;
 
-  for (long long e0 = j_lo; e0 < j_hi; e0 += 32) {
-    const long long e = e0 + lane;
-    const int my_seg = e < j_hi ? __ldg(p.seg + e) : -4;
-    const int my_src = e < j_hi ? __ldg(p.src + e) : 0;
-    const int my_nxt = e + 1 < j_hi ? __ldg(p.seg + e + 1) : (e + 1 == j_hi ? next_seg : -5);
-    const int n_here = (int)min(32LL, j_hi - e0);
-
-#pragma unroll 1
-    for (int rb = 0; rb < RS; rb += U) {
+  for (int sr = 0; sr < C; sr += SR) {
+    const long long base = j_lo + sr;
+    int xr[Q];
+    unsigned endm = 0, validm = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const long long e = base + q * GL + c;
+      const bool ok = e < j_hi;
+      int s = -4, sn = -5, x = 0;
+      if (ok) {
+        s = __ldg(p.seg + e);
+        x = __ldg(p.src + e);
+        sn = e + 1 < t_hi ? __ldg(p.seg + e + 1) : -2;
+      }
+      xr[q] = x;
+      const unsigned be = __ballot_sync(0xffffffffu, ok && s != sn);
+      const unsigned bv = __ballot_sync(0xffffffffu, ok);
+      endm |= ((be >> (g * GL)) & low_bits<GL>()) << (q * GL);
+      validm |= ((bv >> (g * GL)) & low_bits<GL>()) << (q * GL);
+    }
+    if (__ballot_sync(0xffffffffu, validm != 0) == 0) break;
+#pragma unroll
+    for (int m0 = 0; m0 < SR; m0 += U) {
       float4 v[U][NV];
-      int s[U], nx[U];
-      // issue all gathers of the batch first (memory-level parallelism)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = (rb + u) * R + g;
-        s[u] = __shfl_sync(0xffffffffu, my_seg, i);
-        nx[u] = __shfl_sync(0xffffffffu, my_nxt, i);
-        const int x = __shfl_sync(0xffffffffu, my_src, i);
-        const bool ok = i < n_here;
+        const int m = m0 + u;
+        const int x = __shfl_sync(0xffffffffu, xr[m / GL], g * GL + (m % GL));
+        const bool ok = (validm >> m) & 1u;
         const float* row = gbase + (long long)x * gstride;
 #pragma unroll
         for (int w = 0; w < NV; ++w) {
@@ -168,39 +186,29 @@ __device__ __forceinline__ void seg_chunk(const SegParams& p, const DevTable& tb
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int i = (rb + u) * R + g;
-        const bool ok = i < n_here;
-        // segmented inclusive scan across the R groups of this round
+        const int m = m0 + u;
 #pragma unroll
-        for (int off = 1; off < R; off <<= 1) {
-          const int so = __shfl_up_sync(0xffffffffu, s[u], off * GL);
-#pragma unroll
-          for (int w = 0; w < NV; ++w) {
-            const float4 t = shfl4_up(v[u][w], off * GL);
-            if (g >= off && so == s[u]) v[u][w] = f4add(v[u][w], t);
+        for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
+        if ((endm >> m) & 1u) {  // uniform within the group
+          const int s = __ldg(p.seg + base + m);
+          if (s == prev_seg) {
+            // completes a segment that began in an earlier chunk -> fixup
+            store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
+            if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
+          } else {
+            finish_segment<FWD, GL, NV>(p, tb, gmask, s, acc, c, loss_acc);
           }
-        }
-        if (s[u] == carry_seg) {
 #pragma unroll
-          for (int w = 0; w < NV; ++w) v[u][w] = f4add(v[u][w], carry[w]);
+          for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const bool ends = ok && nx[u] != s[u];
-        const bool cont = ok && (e0 + i == j_hi - 1) && nx[u] == s[u];
-        const bool split_left = s[u] == prev_seg;
-        // complete segments: epilogue; split ones: carries for the fixup
-        finish_segment<FWD, GL, NV>(p, tb, ends && !split_left, s[u], v[u], c, loss_acc);
-        if ((ends || cont) && split_left) store_carry<NV>(p, chunk, 0, nvec, GL, c, v[u]);
-        if (cont && !split_left) store_carry<NV>(p, chunk, 1, nvec, GL, c, v[u]);
-        // carry-out from the last group of the round
-        const int lsrc = (R - 1) * GL + c;
-#pragma unroll
-        for (int w = 0; w < NV; ++w) carry[w] = shfl4(v[u][w], lsrc);
-        const int cs = __shfl_sync(0xffffffffu, s[u], lsrc);
-        const bool ce = __shfl_sync(0xffffffffu, (int)ends, lsrc) != 0;
-        carry_seg = ce ? -3 : cs;
       }
     }
   }
+  // The chunk's last segment continues into the next chunk: hand the partial on.
+  if (live && j_hi < t_hi) {
+    const int sl = __ldg(p.seg + j_hi - 1);
+    if (__ldg(p.seg + j_hi) == sl) store_carry<GL, NV>(p, chunk, sl == prev_seg ? 0 : 1, nvec, c, acc);
+  }
   if constexpr (FWD) {
     if (p.loss) {
       float l = loss_acc;
@@ -212,72 +220,103 @@ __device__ __forceinline__ void seg_chunk(const SegParams& p, const DevTable& tb
 }
 
 template <bool FWD>
-__global__ void __launch_bounds__(256) seg_reduce_kernel(SegParams p) {
-  const int chunk = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (chunk >= p.n_chunks) return;
-  const DevTable tb = p.tabs[__ldg(p.chunk_table + chunk)];
+__global__ void __launch_bounds__(256, 3) seg_reduce_kernel(SegParams p) {
+  const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (unit >= p.n_units) return;
+  const int t = __ldg(p.unit_table + unit);
+  const DevTable tb = p.tabs[t];
   switch (tb.kind) {
-    case 0: seg_chunk<FWD, 1, 1>(p, tb, chunk); break;
-    case 1: seg_chunk<FWD, 2, 1>(p, tb, chunk); break;
-    case 2: seg_chunk<FWD, 4, 1>(p, tb, chunk); break;
-    case 3: seg_chunk<FWD, 8, 1>(p, tb, chunk); break;
-    case 4: seg_chunk<FWD, 16, 1>(p, tb, chunk); break;
-    case 5: seg_chunk<FWD, 32, 1>(p, tb, chunk); break;
-    case 6: seg_chunk<FWD, 32, 2>(p, tb, chunk); break;
-    case 7: seg_chunk<FWD, 32, 4>(p, tb, chunk); break;
-    default: seg_chunk<FWD, 32, 8>(p, tb, chunk); break;
+    case 0: seg_unit<FWD, 1, 1>(p, tb, t, unit); break;
+    case 1: seg_unit<FWD, 2, 1>(p, tb, t, unit); break;
+    case 2: seg_unit<FWD, 4, 1>(p, tb, t, unit); break;
+    case 3: seg_unit<FWD, 8, 1>(p, tb, t, unit); break;
+    case 4: seg_unit<FWD, 16, 1>(p, tb, t, unit); break;
+    case 5: seg_unit<FWD, 32, 1>(p, tb, t, unit); break;
+    case 6: seg_unit<FWD, 32, 2>(p, tb, t, unit); break;
+    case 7: seg_unit<FWD, 32, 4>(p, tb, t, unit); break;
+    default: seg_unit<FWD, 32, 8>(p, tb, t, unit); break;
   }
 }
 
-// Fixup: one warp per chunk. The chunk that COMPLETES a segment which began
-// in an earlier chunk sums tail[k0] + head[k0+1..k] in chunk order and runs
-// the epilogue. Whole-warp lane layout: lane owns float4 columns lane+32*w.
+// Fixup: one CTA per completer chunk k. The segment's first element is found
+// by a 32-ary lower_bound on the (sorted) keys, giving its first chunk k0;
+// the partials tail[k0] + head[k0+1..k] are summed by 8 warps over contiguous
+// ranges and combined in warp order (deterministic), then the epilogue runs.
 template <bool FWD>
 __global__ void __launch_bounds__(256) seg_fixup_kernel(SegParams p) {
-  const int chunk = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (chunk >= p.n_chunks) return;
-  const int lane = threadIdx.x & 31;
-  const DevTable tb = p.tabs[__ldg(p.chunk_table + chunk)];
-  const long long t_lo = tb.idx_off, t_hi = tb.idx_off + tb.n_lookups;
-  const long long j_lo = t_lo + (long long)(chunk - tb.chunk_off) * tb.chunk_len;
-  const long long j_hi = min(j_lo + (long long)tb.chunk_len, t_hi);
-  if (j_lo >= j_hi || j_lo == t_lo) return;
-  const int first = __ldg(p.seg + j_lo);
-  if (__ldg(p.seg + j_lo - 1) != first) return;  // not split on the left
-  if (j_hi < t_hi && __ldg(p.seg + j_hi) == first && __ldg(p.seg + j_hi - 1) == first) return;  // middle
-  // find k0: walk back over middle chunks (warp-parallel, 32 chunks per probe)
-  int k0 = -1;
-  for (int base = chunk - 1; k0 < 0; base -= 32) {
-    const int k = base - lane;
-    bool mid = false;
-    if (k >= tb.chunk_off) {
-      const long long jl = t_lo + (long long)(k - tb.chunk_off) * tb.chunk_len;
-      mid = jl > t_lo && __ldg(p.seg + jl - 1) == first;
+  __shared__ float4 part[8][256];
+  __shared__ int s_k0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = *p.n_completers;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int2 ct = p.completers[i];
+    const int chunk = ct.x;
+    const DevTable tb = p.tabs[ct.y];
+    const long long t_lo = tb.idx_off;
+    const long long j_lo = t_lo + (long long)(chunk - tb.chunk_off) * tb.chunk_len;
+    const int first = __ldg(p.seg + j_lo);
+    if (warp == 0) {
+      long long lo = t_lo, hi = j_lo;  // lower_bound(first) in [lo, hi]
+      while (hi - lo > 32) {
+        const long long step = (hi - lo + 31) / 32;
+        const long long q = lo + lane * step;
+        const bool lt = q < hi && __ldg(p.seg + q) < first;
+        const int cnt = __popc(__ballot_sync(0xffffffffu, lt));
+        if (cnt == 0) {
+          hi = lo;
+        } else {
+          const long long last = lo + (long long)(cnt - 1) * step;
+          if (cnt < 32 && lo + (long long)cnt * step < hi) hi = lo + (long long)cnt * step;
+          lo = last + 1;
+        }
+      }
+      const long long q = lo + lane;
+      const bool lt = q < hi && __ldg(p.seg + q) < first;
+      const long long p0 = lo + __popc(__ballot_sync(0xffffffffu, lt));
+      if (lane == 0) s_k0 = tb.chunk_off + (int)((p0 - t_lo) / tb.chunk_len);
     }
-    const unsigned notmid = __ballot_sync(0xffffffffu, !mid);
-    if (notmid) k0 = base - (__ffs(notmid) - 1);
-  }
-  const int nvec = tb.dim >> 2;
-  float4 v[8];
+    __syncthreads();
+    const int k0 = s_k0;
+    const int nparts = chunk - k0 + 1;
+    const int per = (nparts + 7) / 8;
+    const int a = k0 + warp * per, b = min(chunk + 1, a + per);
+    const int nvec = tb.dim >> 2;
+    float4 v[8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) v[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int k = k0; k <= chunk; ++k) {
-    const float* src = p.carry + ((long long)k * 2 + (k == k0 ? 1 : 0)) * p.carry_stride;
+    for (int w = 0; w < 8; ++w) v[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = a; k < b; ++k) {
+      const float* src = p.carry + ((long long)k * 2 + (k == k0 ? 1 : 0)) * p.carry_stride;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const int cv = lane + 32 * w;
-      if (cv < nvec) v[w] = f4add(v[w], *reinterpret_cast<const float4*>(src + cv * 4));
+      for (int w = 0; w < 8; ++w) {
+        const int cv = lane + 32 * w;
+        if (cv < nvec) v[w] = f4add(v[w], *reinterpret_cast<const float4*>(src + cv * 4));
+      }
     }
-  }
-  float loss_acc = 0.f;
-  finish_segment<FWD, 32, 8>(p, tb, true, first, v, lane, loss_acc);
-  if constexpr (FWD) {
-    if (p.loss) {
-      float l = loss_acc;
 #pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
-      if (lane == 0 && l != 0.f) atomicAdd(p.loss, 0.5 * (double)l);
+    for (int w = 0; w < 8; ++w)
+      if (lane + 32 * w < nvec) part[warp][lane + 32 * w] = v[w];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int cv = lane + 32 * w;
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (cv < nvec)
+          for (int k = 0; k < 8; ++k) s = f4add(s, part[k][cv]);
+        v[w] = s;
+      }
+      float loss_acc = 0.f;
+      finish_segment<FWD, 32, 8>(p, tb, 0xffffffffu, first, v, lane, loss_acc);
+      if constexpr (FWD) {
+        if (p.loss) {
+          float l = loss_acc;
+#pragma unroll
+          for (int m = 16; m >= 1; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
+          if (lane == 0 && l != 0.f) atomicAdd(p.loss, 0.5 * (double)l);
+        }
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -348,16 +387,17 @@ __global__ void pack_offsets_kernel(const long long* __restrict__ off64, int T, 
 
 __global__ void __launch_bounds__(256) pack_indices_kernel(const long long* __restrict__ idx64,
                                                            const DevTable* __restrict__ tabs,
-                                                           const int* __restrict__ chunk_table,
-                                                           int n_chunks, int* __restrict__ idx32,
+                                                           const int* __restrict__ unit_table, int n_units,
+                                                           int* __restrict__ idx32,
                                                            unsigned long long* __restrict__ err) {
-  const int chunk = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (chunk >= n_chunks) return;
+  const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (unit >= n_units) return;
   const int lane = threadIdx.x & 31;
-  const int t = chunk_table[chunk];
+  const int t = unit_table[unit];
   const DevTable tb = tabs[t];
-  const long long j_lo = tb.idx_off + (long long)(chunk - tb.chunk_off) * tb.chunk_len;
-  const long long j_hi = min(j_lo + (long long)tb.chunk_len, tb.idx_off + tb.n_lookups);
+  const long long per = (long long)(32 >> (tb.kind < 5 ? tb.kind : 5)) * tb.chunk_len;
+  const long long j_lo = tb.idx_off + (long long)(unit - tb.unit_off) * per;
+  const long long j_hi = min(j_lo + per, tb.idx_off + tb.n_lookups);
   for (long long j = j_lo + lane; j < j_hi; j += 32) {
     const long long v = idx64[j];
     if (v < 0 || v >= tb.hash) {

@@ -1,6 +1,8 @@
 // Plain structs shared by the host context and the kernels.
 #pragma once
 
+#include <vector_types.h>
+
 namespace asb {
 
 // Per-table device descriptor (host-built, see context.cu).
@@ -12,16 +14,18 @@ struct DevTable {
   long long n_lookups;  // L_t of the loaded batch
   int dim;
   int col;        // first pooled column
-  int chunk_off;  // first chunk id
+  int chunk_off;  // first (global) chunk id; a table owns n_units * (32/GL) chunks
   int chunk_len;  // elements per chunk (multiple of 32)
+  int unit_off;   // first warp unit; a warp unit = 32/GL consecutive chunks
+  int n_units;
   int table_id;
   int kind;  // lane layout: 0..5 -> GL = 1<<kind, NV = 1; 6,7,8 -> GL = 32, NV = 2,4,8
 };
 
 struct SegParams {
   const DevTable* tabs;
-  const int* chunk_table;  // chunk -> table position
-  int n_chunks;
+  const int* unit_table;  // warp unit -> table position
+  int n_units;
   const int* seg;  // segment key per element
   const int* src;  // gathered row per element
   // forward
@@ -38,6 +42,9 @@ struct SegParams {
   // carries: [n_chunks][2][carry_stride] (0 = head, 1 = tail)
   float* carry;
   int carry_stride;
+  // chunks completing a segment that began in an earlier chunk: {chunk, table}
+  int2* completers;
+  int* n_completers;
 };
 
 }  // namespace asb
