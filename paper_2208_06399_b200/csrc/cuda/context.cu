@@ -203,10 +203,11 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   stage_off_ = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
-  counters_ = static_cast<int*>(dalloc(sizeof(int) * 2));
+  counters_ = static_cast<int*>(dalloc(sizeof(int) * 4));
   int sms = 148;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
   fixup_grid_ = static_cast<unsigned>(sms * 2);
+  fixup_short_grid_ = static_cast<unsigned>(sms * 16);
   int l2 = 0;
   cuda_check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_), "L2 size");
   flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
@@ -269,9 +270,11 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
     drop(carry_);
     drop(completers_);
+    drop(completers_long_);
     const int64_t cap = std::max<int64_t>(n_chunks + n_chunks / 8, 64);
     carry_ = static_cast<float*>(dalloc(sizeof(float) * cap * 2 * max_dim_));
     completers_ = static_cast<int2*>(dalloc(sizeof(int2) * cap));
+    completers_long_ = static_cast<int4*>(dalloc(sizeof(int4) * cap));
     cap_chunks_ = cap;
   }
   if (n_units > cap_units_) {
@@ -373,7 +376,9 @@ SegParams EmbContext::seg_params(bool fwd) const {
   p.unit_table = unit_table_;
   p.n_units = static_cast<int>(n_units_);
   p.completers = completers_;
-  p.n_completers = counters_ + (fwd ? 0 : 1);
+  p.n_completers = counters_ + (fwd ? 0 : 2);
+  p.completers_long = completers_long_;
+  p.n_completers_long = counters_ + (fwd ? 1 : 3);
   p.seg = fwd ? bag_ : skey_;
   p.src = fwd ? idx32_ : sbag_;
   p.carry = carry_;
@@ -401,7 +406,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.out_stride = sum_dim_;
   p.loss = loss_dev;
   const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
-  cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int), s), "counter reset");
+  cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 1, s);
     seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
@@ -409,10 +414,11 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   }
   {
     Phase ph(this, 2, s);
-    seg_fixup_kernel<true><<<fixup_grid_, kBlock, 0, s>>>(p);
+    seg_fixup_kernel<true><<<fixup_short_grid_, kBlock, 0, s>>>(p);
+    seg_fixup_long_kernel<true><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
   }
-  launches_ += 2;
+  launches_ += 3;
 }
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
@@ -437,7 +443,7 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   p.lr = lr;
   p.eps = eps;
   const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
-  cuda_check(cudaMemsetAsync(counters_ + 1, 0, sizeof(int), s), "counter reset");
+  cuda_check(cudaMemsetAsync(counters_ + 2, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 4, s);
     seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
@@ -445,10 +451,11 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   }
   {
     Phase ph(this, 5, s);
-    seg_fixup_kernel<false><<<fixup_grid_, kBlock, 0, s>>>(p);
+    seg_fixup_kernel<false><<<fixup_short_grid_, kBlock, 0, s>>>(p);
+    seg_fixup_long_kernel<false><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
   }
-  launches_ += 2;
+  launches_ += 3;
 }
 
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
@@ -572,7 +579,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 5 + 2 + (end_bit_ + 7) / 8);
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + (end_bit_ + 7) / 8);
 }
 
 }  // namespace asb

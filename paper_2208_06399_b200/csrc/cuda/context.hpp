@@ -80,8 +80,10 @@ class EmbContext {
   long long* stage_idx_ = nullptr;
   int* unit_table_ = nullptr;
   int2* completers_ = nullptr;
-  int* counters_ = nullptr;  // [0] fwd completers, [1] bwd completers
+  int4* completers_long_ = nullptr;
+  int* counters_ = nullptr;  // [0,1] fwd completers (short, long), [2,3] bwd
   unsigned fixup_grid_ = 296;
+  unsigned fixup_short_grid_ = 2368;
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
   float* carry_ = nullptr;

@@ -238,58 +238,145 @@ __global__ void __launch_bounds__(256, 3) seg_reduce_kernel(SegParams p) {
   }
 }
 
-// Fixup: one CTA per completer chunk k. The segment's first element is found
-// by a 32-ary lower_bound on the (sorted) keys, giving its first chunk k0;
-// the partials tail[k0] + head[k0+1..k] are summed by 8 warps over contiguous
-// ranges and combined in warp order (deterministic), then the epilogue runs.
+// ---- fixups -----------------------------------------------------------------
+// A completer chunk k finishes a segment that began in an earlier chunk k0;
+// its value is tail[k0] + head[k0+1] + ... + head[k] (fixed order).
+// k0 = k-1 is the common case (checked with one load); otherwise a 32-ary
+// lower_bound over the sorted keys finds the segment's first element.
+// Segments spanning <= kShortParts chunks are finished by one warp; longer
+// ones (hot rows, very long bags) are queued for a CTA-wide reduction.
+constexpr int kShortParts = 64;
+
+__device__ __forceinline__ int find_k0(const SegParams& p, const DevTable& tb, int chunk, int first, int lane) {
+  const long long t_lo = tb.idx_off;
+  const long long jp = t_lo + (long long)(chunk - 1 - tb.chunk_off) * tb.chunk_len;  // start of chunk k-1
+  if (jp == t_lo || __ldg(p.seg + jp - 1) != first) return chunk - 1;
+  long long lo = t_lo, hi = jp - 1;  // lower_bound(first) lies in [lo, hi]
+  while (hi - lo > 32) {
+    const long long step = (hi - lo + 31) / 32;
+    const long long q = lo + lane * step;
+    const bool lt = q < hi && __ldg(p.seg + q) < first;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, lt));
+    if (cnt == 0) {
+      hi = lo;
+    } else {
+      if (cnt < 32 && lo + (long long)cnt * step < hi) hi = lo + (long long)cnt * step;
+      lo = lo + (long long)(cnt - 1) * step + 1;
+    }
+  }
+  const long long q = lo + lane;
+  const bool lt = q < hi && __ldg(p.seg + q) < first;
+  const long long p0 = lo + __popc(__ballot_sync(0xffffffffu, lt));
+  return tb.chunk_off + (int)((p0 - t_lo) / tb.chunk_len);
+}
+
+__device__ __forceinline__ const float* carry_of(const SegParams& p, int k, int k0) {
+  return p.carry + ((long long)k * 2 + (k == k0 ? 1 : 0)) * p.carry_stride;
+}
+
+template <bool FWD>
+__device__ __forceinline__ void fixup_loss(const SegParams& p, float loss_acc, int lane) {
+  if constexpr (FWD) {
+    if (p.loss) {
+      float l = loss_acc;
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
+      if (lane == 0 && l != 0.f) atomicAdd(p.loss, 0.5 * (double)l);
+    }
+  }
+}
+
+// Warp per completer. Whole-warp lane layout: lane owns float4 columns lane + 32*w.
 template <bool FWD>
 __global__ void __launch_bounds__(256) seg_fixup_kernel(SegParams p) {
-  __shared__ float4 part[8][256];
-  __shared__ int s_k0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int n = *p.n_completers;
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  float loss_acc = 0.f;
+  for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += gridDim.x * 8) {
     const int2 ct = p.completers[i];
     const int chunk = ct.x;
     const DevTable tb = p.tabs[ct.y];
-    const long long t_lo = tb.idx_off;
-    const long long j_lo = t_lo + (long long)(chunk - tb.chunk_off) * tb.chunk_len;
-    const int first = __ldg(p.seg + j_lo);
-    if (warp == 0) {
-      long long lo = t_lo, hi = j_lo;  // lower_bound(first) in [lo, hi]
-      while (hi - lo > 32) {
-        const long long step = (hi - lo + 31) / 32;
-        const long long q = lo + lane * step;
-        const bool lt = q < hi && __ldg(p.seg + q) < first;
-        const int cnt = __popc(__ballot_sync(0xffffffffu, lt));
-        if (cnt == 0) {
-          hi = lo;
-        } else {
-          const long long last = lo + (long long)(cnt - 1) * step;
-          if (cnt < 32 && lo + (long long)cnt * step < hi) hi = lo + (long long)cnt * step;
-          lo = last + 1;
-        }
-      }
-      const long long q = lo + lane;
-      const bool lt = q < hi && __ldg(p.seg + q) < first;
-      const long long p0 = lo + __popc(__ballot_sync(0xffffffffu, lt));
-      if (lane == 0) s_k0 = tb.chunk_off + (int)((p0 - t_lo) / tb.chunk_len);
+    const int first = __ldg(p.seg + tb.idx_off + (long long)(chunk - tb.chunk_off) * tb.chunk_len);
+    const int k0 = find_k0(p, tb, chunk, first, lane);
+    if (chunk - k0 + 1 > kShortParts) {
+      if (lane == 0) p.completers_long[atomicAdd(p.n_completers_long, 1)] = make_int4(chunk, ct.y, k0, first);
+      continue;
     }
-    __syncthreads();
-    const int k0 = s_k0;
-    const int nparts = chunk - k0 + 1;
-    const int per = (nparts + 7) / 8;
-    const int a = k0 + warp * per, b = min(chunk + 1, a + per);
     const int nvec = tb.dim >> 2;
     float4 v[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) v[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = a; k < b; ++k) {
-      const float* src = p.carry + ((long long)k * 2 + (k == k0 ? 1 : 0)) * p.carry_stride;
+    if (nvec <= 32) {
+      const bool on = lane < nvec;
+      int k = k0;
+      for (; k + 4 <= chunk + 1; k += 4) {  // 4 carries in flight
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        if (on) {
+          a0 = *reinterpret_cast<const float4*>(carry_of(p, k, k0) + lane * 4);
+          a1 = *reinterpret_cast<const float4*>(carry_of(p, k + 1, k0) + lane * 4);
+          a2 = *reinterpret_cast<const float4*>(carry_of(p, k + 2, k0) + lane * 4);
+          a3 = *reinterpret_cast<const float4*>(carry_of(p, k + 3, k0) + lane * 4);
+        }
+        v[0] = f4add(f4add(f4add(f4add(v[0], a0), a1), a2), a3);
+      }
+      for (; k <= chunk; ++k)
+        if (on) v[0] = f4add(v[0], *reinterpret_cast<const float4*>(carry_of(p, k, k0) + lane * 4));
+    } else {
+      for (int k = k0; k <= chunk; ++k) {
+        const float* src = carry_of(p, k, k0);
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int cv = lane + 32 * w;
-        if (cv < nvec) v[w] = f4add(v[w], *reinterpret_cast<const float4*>(src + cv * 4));
+        for (int w = 0; w < 8; ++w) {
+          const int cv = lane + 32 * w;
+          if (cv < nvec) v[w] = f4add(v[w], *reinterpret_cast<const float4*>(src + cv * 4));
+        }
+      }
+    }
+    finish_segment<FWD, 32, 8>(p, tb, 0xffffffffu, first, v, lane, loss_acc);
+  }
+  fixup_loss<FWD>(p, loss_acc, lane);
+}
+
+// CTA per long segment: 8 warps sum contiguous ranges of the partials, then
+// warp 0 combines them in warp order and runs the epilogue.
+template <bool FWD>
+__global__ void __launch_bounds__(256) seg_fixup_long_kernel(SegParams p) {
+  __shared__ float4 part[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = *p.n_completers_long;
+  float loss_acc = 0.f;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int4 ct = p.completers_long[i];
+    const int chunk = ct.x, k0 = ct.z, first = ct.w;
+    const DevTable tb = p.tabs[ct.y];
+    const int nvec = tb.dim >> 2;
+    const int nparts = chunk - k0 + 1;
+    const int per = (nparts + 7) / 8;
+    const int a = k0 + warp * per, b = min(chunk + 1, a + per);
+    float4 v[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nvec <= 32) {
+      const bool on = lane < nvec;
+      int k = a;
+      for (; k + 8 <= b; k += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          x[u] = on ? *reinterpret_cast<const float4*>(carry_of(p, k + u, k0) + lane * 4)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[0] = f4add(v[0], x[u]);
+      }
+      for (; k < b; ++k)
+        if (on) v[0] = f4add(v[0], *reinterpret_cast<const float4*>(carry_of(p, k, k0) + lane * 4));
+    } else {
+      for (int k = a; k < b; ++k) {
+        const float* src = carry_of(p, k, k0);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int cv = lane + 32 * w;
+          if (cv < nvec) v[w] = f4add(v[w], *reinterpret_cast<const float4*>(src + cv * 4));
+        }
       }
     }
 #pragma unroll
@@ -302,22 +389,14 @@ __global__ void __launch_bounds__(256) seg_fixup_kernel(SegParams p) {
         const int cv = lane + 32 * w;
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
         if (cv < nvec)
-          for (int k = 0; k < 8; ++k) s = f4add(s, part[k][cv]);
+          for (int q = 0; q < 8; ++q) s = f4add(s, part[q][cv]);
         v[w] = s;
       }
-      float loss_acc = 0.f;
       finish_segment<FWD, 32, 8>(p, tb, 0xffffffffu, first, v, lane, loss_acc);
-      if constexpr (FWD) {
-        if (p.loss) {
-          float l = loss_acc;
-#pragma unroll
-          for (int m = 16; m >= 1; m >>= 1) l += __shfl_xor_sync(0xffffffffu, l, m);
-          if (lane == 0 && l != 0.f) atomicAdd(p.loss, 0.5 * (double)l);
-        }
-      }
     }
     __syncthreads();
   }
+  if (warp == 0) fixup_loss<FWD>(p, loss_acc, lane);
 }
 
 // K4: bag id per lookup from the offsets; empty bags get a zero pooled row

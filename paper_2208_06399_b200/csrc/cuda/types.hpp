@@ -45,6 +45,9 @@ struct SegParams {
   // chunks completing a segment that began in an earlier chunk: {chunk, table}
   int2* completers;
   int* n_completers;
+  // completers of long segments: {chunk, table, k0, key}
+  int4* completers_long;
+  int* n_completers_long;
 };
 
 }  // namespace asb

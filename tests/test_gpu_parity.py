@@ -4,8 +4,12 @@ Tolerances:
 * forward: BIT-EXACT. Initial weights live on the grid k*2^-12 (|k| <= 512), so
   every partial sum of a bag below 2^12 in magnitude is exact in fp32 whatever
   the summation order; the fp64 oracle must therefore match exactly.
-* backward / updated rows and momentum: |gpu - ref| <= 1e-5*|ref| + 1e-7
-  (north star: 1e-5 relative fp32), ref in fp64.
+* backward / updated rows: |gpu - ref| <= 1e-5*max(|ref|, |W_old|, |W_old - ref|) + 1e-7
+  elementwise (north star: 1e-5 relative fp32; the scale is that of the terms
+  of W_old - update, so cancellation to ~0 does not demand more than fp32
+  delivers). Momentum: |gpu - ref| <= 1e-5*|ref| + 1e-7. ref in fp64. Gradients
+  of rows hit > 2^12 times exceed the exact fp32 grid, so fp32 accumulation
+  order matters there; the bound above covers it.
 * index handling (bag segmentation, sorted unique rows, counts): bit-exact.
 """
 import numpy as np
@@ -29,7 +33,9 @@ def run_bwd_check(oracle, shard, tables, streams, grad, seed, B):
         if len(r["rows"]) == 0:
             continue
         w = shard.read_rows(t, r["rows"])
-        ok, worst = fp_close(w, r["w"])
+        w_old = weight_rows(seed, tab.id, r["rows"], tab.dim).astype(np.float64)
+        scale = np.maximum(np.abs(w_old), np.abs(w_old - r["w"]))
+        ok, worst = fp_close(w, r["w"], scale=scale)
         assert ok, f"table {tab.id}: updated rows off by {worst:.3g}x tolerance"
         m = shard.read_momentum(t, r["rows"])
         ok, worst = fp_close(m, r["m"])
@@ -168,11 +174,13 @@ def test_multistep_dense_against_oracle(P, oracle, cuda):
             assert ok, f"step {step}: forward off by {worst:.3g}x tolerance"
             sh.backward(None, LR, EPS)
             grad = ref.astype(np.float32)
+            W_old = [w.copy() for w in W]
             for t in range(len(pool)):
                 oracle.backward_adagrad_f64(ot[t], B, *st[t], grad, sh.cols[t], LR, EPS, W=W[t], M=M[t])
             for t, tab in enumerate(pool):
                 allrows = np.arange(tab.hash_size)
-                ok, worst = fp_close(sh.read_rows(t, allrows), W[t], rtol=1e-5, atol=1e-6)
+                scale = np.maximum(np.abs(W_old[t]), np.abs(W_old[t] - W[t]))
+                ok, worst = fp_close(sh.read_rows(t, allrows), W[t], rtol=1e-5, atol=1e-6, scale=scale)
                 assert ok, f"step {step} table {tab.id}: weights off by {worst:.3g}x"
 
 
