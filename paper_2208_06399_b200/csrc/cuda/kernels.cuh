@@ -110,15 +110,24 @@ __device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int w
 
 // One warp = one "unit" = 32/GL consecutive chunks of one table; each group
 // of GL lanes walks its own chunk sequentially: gather a row, add it to the
-// running sum, finish the segment when the key changes. Per element a lane
-// issues one shuffle (row id), one 16-byte gather per float4 column and the
-// adds; the segment-end test is a bit of a group mask built with ballots.
+// running sum, finish the segment when the key changes.
+//
+// Per 32-element super-round a group stages its elements' row ids and keys in
+// shared memory (one coalesced load per lane) and builds 32-bit "segment ends
+// here" / "valid" masks with ballots. The gathers are issued U at a time
+// (U x 16 B in flight per lane); a batch without a segment end is a plain
+// run of adds, a batch with ends walks them with __ffs and ONE copy of the
+// epilogue, which keeps the kernel small enough for the instruction cache.
+constexpr int kSegWarps = 8;   // warps per CTA of the segment kernels
+constexpr int kStage = 256;    // staged elements per warp per super-round
+
 template <bool FWD, int GL, int NV>
-__device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit) {
-  constexpr int R = 32 / GL;                     // chunks (groups) per warp
+__device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
+  constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
-  constexpr int Q = SR / GL;                     // elements held per lane per super-round
-  constexpr int U = NV >= 8 ? 1 : 8 / NV;        // gathers in flight per lane
+  constexpr int Q = SR / GL;                       // elements loaded per lane per super-round
+  constexpr int U = NV >= 8 ? 1 : 8 / NV;          // gathers in flight per lane
+  static_assert(R * SR <= kStage, "stage too small");
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
   const int c = lane % GL;
@@ -132,6 +141,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const long long j_hi = min(j_lo + (long long)C, t_hi);
   const bool live = j_lo < j_hi;
   const int prev_seg = (live && j_lo > t_lo) ? __ldg(p.seg + j_lo - 1) : -1;
+  int* gx = xs + g * SR;
+  int* gs = ss + g * SR;
 
   const float* gbase;
   long long gstride;
@@ -148,9 +159,9 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
   float loss_acc = 0.f;
 
+#pragma unroll 1
   for (int sr = 0; sr < C; sr += SR) {
     const long long base = j_lo + sr;
-    int xr[Q];
     unsigned endm = 0, validm = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -162,35 +173,46 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
         x = __ldg(p.src + e);
         sn = e + 1 < t_hi ? __ldg(p.seg + e + 1) : -2;
       }
-      xr[q] = x;
+      gx[q * GL + c] = x;
+      gs[q * GL + c] = s;
       const unsigned be = __ballot_sync(0xffffffffu, ok && s != sn);
       const unsigned bv = __ballot_sync(0xffffffffu, ok);
       endm |= ((be >> (g * GL)) & low_bits<GL>()) << (q * GL);
       validm |= ((bv >> (g * GL)) & low_bits<GL>()) << (q * GL);
     }
+    __syncwarp();
     if (__ballot_sync(0xffffffffu, validm != 0) == 0) break;
-#pragma unroll
+#pragma unroll 1
     for (int m0 = 0; m0 < SR; m0 += U) {
       float4 v[U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int m = m0 + u;
-        const int x = __shfl_sync(0xffffffffu, xr[m / GL], g * GL + (m % GL));
         const bool ok = (validm >> m) & 1u;
-        const float* row = gbase + (long long)x * gstride;
+        const float* row = gbase + (long long)gx[m] * gstride;
 #pragma unroll
         for (int w = 0; w < NV; ++w) {
           const int cv = c + w * GL;
           v[u][w] = (ok && cv < nvec) ? ldg4(row + cv * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+      unsigned ebits = (endm >> m0) & low_bits<U>();
+      if (ebits == 0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int m = m0 + u;
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
-        if ((endm >> m) & 1u) {  // uniform within the group
-          const int s = __ldg(p.seg + base + m);
+          for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
+      } else {
+        int u0 = 0;
+        for (;;) {  // group-uniform
+          const int e = ebits ? __ffs(ebits) - 1 : U;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (u >= u0 && u <= e)
+#pragma unroll
+              for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
+          if (e >= U) break;
+          const int s = gs[m0 + e];
           if (s == prev_seg) {
             // completes a segment that began in an earlier chunk -> fixup
             store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
@@ -200,9 +222,12 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           }
 #pragma unroll
           for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ebits &= ebits - 1;
+          u0 = e + 1;
         }
       }
     }
+    __syncwarp();
   }
   // The chunk's last segment continues into the next chunk: hand the partial on.
   if (live && j_hi < t_hi) {
@@ -221,20 +246,25 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 
 template <bool FWD>
 __global__ void __launch_bounds__(256, 3) seg_reduce_kernel(SegParams p) {
-  const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
+  __shared__ int xs[kSegWarps][kStage];
+  __shared__ int ss[kSegWarps][kStage];
+  const int warp = threadIdx.x >> 5;
+  const int unit = blockIdx.x * kSegWarps + warp;
   if (unit >= p.n_units) return;
   const int t = __ldg(p.unit_table + unit);
   const DevTable tb = p.tabs[t];
+  int* x = xs[warp];
+  int* s = ss[warp];
   switch (tb.kind) {
-    case 0: seg_unit<FWD, 1, 1>(p, tb, t, unit); break;
-    case 1: seg_unit<FWD, 2, 1>(p, tb, t, unit); break;
-    case 2: seg_unit<FWD, 4, 1>(p, tb, t, unit); break;
-    case 3: seg_unit<FWD, 8, 1>(p, tb, t, unit); break;
-    case 4: seg_unit<FWD, 16, 1>(p, tb, t, unit); break;
-    case 5: seg_unit<FWD, 32, 1>(p, tb, t, unit); break;
-    case 6: seg_unit<FWD, 32, 2>(p, tb, t, unit); break;
-    case 7: seg_unit<FWD, 32, 4>(p, tb, t, unit); break;
-    default: seg_unit<FWD, 32, 8>(p, tb, t, unit); break;
+    case 0: seg_unit<FWD, 1, 1>(p, tb, t, unit, x, s); break;
+    case 1: seg_unit<FWD, 2, 1>(p, tb, t, unit, x, s); break;
+    case 2: seg_unit<FWD, 4, 1>(p, tb, t, unit, x, s); break;
+    case 3: seg_unit<FWD, 8, 1>(p, tb, t, unit, x, s); break;
+    case 4: seg_unit<FWD, 16, 1>(p, tb, t, unit, x, s); break;
+    case 5: seg_unit<FWD, 32, 1>(p, tb, t, unit, x, s); break;
+    case 6: seg_unit<FWD, 32, 2>(p, tb, t, unit, x, s); break;
+    case 7: seg_unit<FWD, 32, 4>(p, tb, t, unit, x, s); break;
+    default: seg_unit<FWD, 32, 8>(p, tb, t, unit, x, s); break;
   }
 }
 
