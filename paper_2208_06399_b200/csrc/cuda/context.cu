@@ -54,11 +54,11 @@ int kind_for_dim(int dim) {
   return 8;
 }
 
-// Elements per chunk: ~64 KB of gathered rows per warp, multiple of 32.
-int chunk_len_for_dim(int dim) {
-  int c = 65536 / (dim * 4);
+// Elements per chunk: ~target bytes of gathered rows per group, multiple of 32.
+int chunk_len_for(int dim, double target_bytes) {
+  int c = static_cast<int>(target_bytes / (dim * 4.0));
   c = (c / 32) * 32;
-  return std::max(32, std::min(4096, c));
+  return std::max(32, std::min(8192, c));
 }
 
 int bit_width_u64(uint64_t x) {
@@ -182,7 +182,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     d.col = static_cast<int>(sum_dim_);
     d.table_id = s.id;
     d.kind = kind_for_dim(s.dim);
-    d.chunk_len = chunk_len_for_dim(s.dim);
+    d.chunk_len = chunk_len_for(s.dim, 131072.0);
     total_rows_ += s.hash_size;
     w_off += s.hash_size * s.dim;
     sum_dim_ += s.dim;
@@ -213,6 +213,10 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
   flush_ = dalloc(flush_bytes_);
 
+  cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+
   // K6: weights from the counter hash, momentum zero.
   const unsigned long long s0 = splitmix64(seed_);
   int64_t off = 0;
@@ -239,6 +243,9 @@ EmbContext::~EmbContext() {
     cudaEventDestroy(u.second.second);
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
+  if (side_) cudaStreamDestroy(side_);
+  if (ev_fork_) cudaEventDestroy(ev_fork_);
+  if (ev_join_) cudaEventDestroy(ev_join_);
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -290,6 +297,16 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
                       cudaStream_t s) {
   DeviceGuard g(device_);
   loaded_ = false;
+  if (sort_pending_) {  // a forward's side-stream sort may still read the old batch
+    cuda_check(cudaStreamSynchronize(side_), "side sync");
+    sort_pending_ = false;
+  }
+  // Chunk length: ~128 KB of gathered rows per group, shrunk for small
+  // batches so that there is at least about one wave of warps.
+  double gbytes = 0.0;
+  for (int t = 0; t < T_; ++t) gbytes += 4.0 * specs_[t].dim * (double)std::max<int64_t>(n_idx[t], 0);
+  const double target = std::max(2048.0, std::min(131072.0, gbytes / (148.0 * 24.0)));
+  for (int t = 0; t < T_; ++t) htabs_[t].chunk_len = chunk_len_for(specs_[t].dim, target);
   int64_t L = 0, nch = 0, nun = 0;
   for (int t = 0; t < T_; ++t) {
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
@@ -400,6 +417,11 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
     ++launches_;
   }
   if (n_chunks_ == 0) return;
+  cuda_check(cudaEventRecord(ev_fork_, s), "fork");
+  cuda_check(cudaStreamWaitEvent(side_, ev_fork_, 0), "fork wait");
+  launch_sort(side_);
+  cuda_check(cudaEventRecord(ev_join_, side_), "join");
+  sort_pending_ = true;
   SegParams p = seg_params(true);
   p.W_ro = W_;
   p.out = target;
@@ -421,19 +443,30 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   launches_ += 3;
 }
 
+// K2: stable radix sort of (global row, bag) pairs. Depends only on the
+// loaded batch and the bag ids of K4, so as_forward launches it on a side
+// stream right after K4 where it overlaps the forward gather; the backward
+// joins on it (or sorts inline when no forward ran since the load).
+void EmbContext::launch_sort(cudaStream_t s) {
+  size_t tmp = cub_bytes_;
+  Phase ph(this, 3, s);
+  cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_),
+                                                          reinterpret_cast<unsigned*>(skey_), bag_, sbag_, (int)L_, 0,
+                                                          end_bit_, s),
+             "cub SortPairs");
+  // onesweep: histogram + exclusive-sum + one pass per 8 key bits
+  launches_ += 2 + (end_bit_ + 7) / 8;
+}
+
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
   require_loaded("as_backward_rowwise_adagrad");
   DeviceGuard g(device_);
   if (T_ == 0 || n_chunks_ == 0) return;
-  size_t tmp = cub_bytes_;
-  {
-  Phase ph(this, 3, s);
-  cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_),
-                                             reinterpret_cast<unsigned*>(skey_), bag_, sbag_, (int)L_, 0,
-                                             end_bit_, s),
-             "cub SortPairs");
-  // onesweep: histogram + exclusive-sum + one pass per 8 key bits
-  launches_ += 2 + (end_bit_ + 7) / 8;
+  if (sort_pending_) {
+    cuda_check(cudaStreamWaitEvent(s, ev_join_, 0), "join sort");
+    sort_pending_ = false;
+  } else {
+    launch_sort(s);
   }
   SegParams p = seg_params(false);
   p.grad = grad ? grad : out_;

@@ -49,6 +49,7 @@ class EmbContext {
   void ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units);
   void* dalloc(size_t bytes);
   SegParams seg_params(bool fwd) const;
+  void launch_sort(cudaStream_t s);
 
   int device_;
   int T_;
@@ -90,6 +91,9 @@ class EmbContext {
   void* cub_tmp_ = nullptr;
   size_t cub_bytes_ = 0;
 
+  cudaStream_t side_ = nullptr;  // K2 sort overlapped with the forward
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  bool sort_pending_ = false;
   int64_t L_ = 0;
   int64_t n_chunks_ = 0;
   bool loaded_ = false;

@@ -126,14 +126,18 @@ def test_long_bags_hot_rows_empty_tables(P, oracle, cuda, dim):
     empty bags, bags exactly one chunk long, and a table with no lookups."""
     B = 64
     rng = np.random.default_rng(0)
-    chunk = max(32, min(4096, (65536 // (dim * 4)) // 32 * 32))
+    hash_sizes = [5000, 70, 10, 1000]
+    # the device's chunk length for this batch (context.cu chunk_len_for): bags of
+    # exactly one / two chunks and chunk-1 / chunk+1 exercise every carry case
+    est = 4.0 * dim * (20000 + 4 * 2048 + 5000 + 50 * B)
+    target = max(2048.0, min(131072.0, est / (148.0 * 24.0)))
+    chunk = max(32, min(8192, int(target / (dim * 4.0)) // 32 * 32))
     lens = [
         np.array([0, 20000, 1, 0, 0, chunk, chunk, 2 * chunk + 1] + [3] * (B - 8)),
         np.array([chunk - 1, 1, chunk + 1] + [0] * (B - 4) + [5000]),
         np.zeros(B, dtype=np.int64),
         rng.integers(0, 50, size=B),
     ]
-    hash_sizes = [5000, 70, 10, 1000]
 
     def rows(t, n):
         if t == 1:
