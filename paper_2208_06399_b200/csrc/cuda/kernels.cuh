@@ -54,46 +54,75 @@ __device__ __forceinline__ float group_sum(float x, unsigned mask) {
   return x;
 }
 
-// Segment epilogue, executed by the GL lanes of one group.
-//   forward : pooled[bag, col_t + :] = v            (+ loss 1/2|v|^2)
-//   backward: m_r += |g|^2/D; W_r -= lr * g / (sqrt(m_r) + eps)   (FBGEMM exact row-wise Adagrad)
+// Segment epilogues, executed by the GL lanes of one group.
+// forward : pooled[bag, col_t + :] = v   (+ loss 1/2|v|^2)
+template <int GL, int NV>
+__device__ __forceinline__ void store_pooled(const SegParams& p, const DevTable& tb, int seg, const float4 (&v)[NV],
+                                             int c, float& loss_acc) {
+  const int nvec = tb.dim >> 2;
+  float* o = p.out + (long long)seg * p.out_stride + tb.col;
+#pragma unroll
+  for (int w = 0; w < NV; ++w) {
+    const int cv = c + w * GL;
+    if (cv < nvec) {
+      st4_streaming(o + cv * 4, v[w]);
+      loss_acc += f4dot(v[w]);
+    }
+  }
+}
+
+template <int GL, int NV>
+__device__ __forceinline__ void load_row_state(const SegParams& p, const DevTable& tb, int seg, int c,
+                                               float4 (&w)[NV], float& m) {
+  const int nvec = tb.dim >> 2;
+  const float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
+  m = p.M[seg];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const int cv = c + q * GL;
+    w[q] = cv < nvec ? *reinterpret_cast<const float4*>(wr + cv * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// backward: m_r += |g|^2/D; W_r -= lr * g / (sqrt(m_r) + eps)  (FBGEMM exact row-wise Adagrad).
+// w / m_old: the row's current weights and momentum (prefetched by the caller).
+template <int GL, int NV>
+__device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& tb, unsigned gmask, int seg,
+                                            const float4 (&g)[NV], int c, const float4 (&w)[NV], float m_old) {
+  const int nvec = tb.dim >> 2;
+  float sq = 0.f;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    if (c + q * GL < nvec) sq += f4dot(g[q]);
+  sq = group_sum<GL>(sq, gmask);
+  const float m = m_old + sq / (float)tb.dim;
+  const float mult = p.lr / (sqrtf(m) + p.eps);
+  float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const int cv = c + q * GL;
+    if (cv < nvec) {
+      float4 x = w[q];
+      x.x -= mult * g[q].x;
+      x.y -= mult * g[q].y;
+      x.z -= mult * g[q].z;
+      x.w -= mult * g[q].w;
+      *reinterpret_cast<float4*>(wr + cv * 4) = x;
+    }
+  }
+  if (c == 0) p.M[seg] = m;
+}
+
 template <bool FWD, int GL, int NV>
 __device__ __forceinline__ void finish_segment(const SegParams& p, const DevTable& tb, unsigned gmask, int seg,
                                                const float4 (&v)[NV], int c, float& loss_acc) {
-  const int nvec = tb.dim >> 2;
   if constexpr (FWD) {
-    float* o = p.out + (long long)seg * p.out_stride + tb.col;
-#pragma unroll
-    for (int w = 0; w < NV; ++w) {
-      const int cv = c + w * GL;
-      if (cv < nvec) {
-        st4_streaming(o + cv * 4, v[w]);
-        loss_acc += f4dot(v[w]);
-      }
-    }
+    store_pooled<GL, NV>(p, tb, seg, v, c, loss_acc);
   } else {
-    float sq = 0.f;
-#pragma unroll
-    for (int w = 0; w < NV; ++w)
-      if (c + w * GL < nvec) sq += f4dot(v[w]);
-    sq = group_sum<GL>(sq, gmask);
-    const float m = p.M[seg] + sq / (float)tb.dim;
-    const float mult = p.lr / (sqrtf(m) + p.eps);
-    float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
-#pragma unroll
-    for (int w = 0; w < NV; ++w) {
-      const int cv = c + w * GL;
-      if (cv < nvec) {
-        float4* q = reinterpret_cast<float4*>(wr + cv * 4);
-        float4 x = *q;
-        x.x -= mult * v[w].x;
-        x.y -= mult * v[w].y;
-        x.z -= mult * v[w].z;
-        x.w -= mult * v[w].w;
-        *q = x;
-      }
-    }
-    if (c == 0) p.M[seg] = m;
+    float4 w[NV];
+    float m;
+    load_row_state<GL, NV>(p, tb, seg, c, w, m);
+    adagrad_row<GL, NV>(p, tb, gmask, seg, v, c, w, m);
   }
 }
 
@@ -108,26 +137,40 @@ __device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int w
   }
 }
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // One warp = one "unit" = 32/GL consecutive chunks of one table; each group
 // of GL lanes walks its own chunk sequentially: gather a row, add it to the
 // running sum, finish the segment when the key changes.
 //
-// Per 32-element super-round a group stages its elements' row ids and keys in
-// shared memory (one coalesced load per lane) and builds 32-bit "segment ends
-// here" / "valid" masks with ballots. The gathers are issued U at a time
-// (U x 16 B in flight per lane); a batch without a segment end is a plain
-// run of adds, a batch with ends walks them with __ffs and ONE copy of the
-// epilogue, which keeps the kernel small enough for the instruction cache.
-constexpr int kSegWarps = 8;   // warps per CTA of the segment kernels
-constexpr int kStage = 256;    // staged elements per warp per super-round
+// Row ids and keys of each 32-element super-round are staged in shared
+// memory with cp.async, double-buffered (the next super-round's indices are
+// in flight while this one is gathered). Gathers are issued U at a time
+// (U x 16 B per lane in flight, address = base + row * stride in one
+// IMAD.WIDE.U32); a batch without a segment end is a plain run of adds, a
+// batch with ends walks them with __ffs and ONE copy of the epilogue (small
+// SASS, fits the instruction cache). The backward prefetches the weight row
+// and momentum of the first segment ending in a batch together with the
+// batch's gradient gathers.
+constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
+constexpr int kStageX = 256;  // staged row ids per warp per buffer (R * SR)
+constexpr int kStageS = 288;  // staged keys per warp per buffer (R * (SR + 1))
 
 template <bool FWD, int GL, int NV>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
-  constexpr int Q = SR / GL;                       // elements loaded per lane per super-round
+  constexpr int Q = SR / GL;                       // elements staged per lane per super-round
   constexpr int U = NV >= 8 ? 1 : 8 / NV;          // gathers in flight per lane
-  static_assert(R * SR <= kStage, "stage too small");
+  static_assert(R * SR <= kStageX && R * (SR + 1) <= kStageS, "stage too small");
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
   const int c = lane % GL;
@@ -141,62 +184,96 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const long long j_hi = min(j_lo + (long long)C, t_hi);
   const bool live = j_lo < j_hi;
   const int prev_seg = (live && j_lo > t_lo) ? __ldg(p.seg + j_lo - 1) : -1;
-  int* gx = xs + g * SR;
-  int* gs = ss + g * SR;
 
   const float* gbase;
-  long long gstride;
+  unsigned gstride;
   if constexpr (FWD) {
     gbase = p.W_ro + tb.w_base;
-    gstride = tb.dim;
+    gstride = (unsigned)tb.dim;
   } else {
     gbase = p.grad + tb.col;
-    gstride = p.grad_stride;
+    gstride = (unsigned)p.grad_stride;
   }
+  gbase += c * 4;
+
+  // stage the row ids [base, base+SR) and keys [base, base+SR] of one super-round
+  auto stage = [&](long long base, int buf) {
+    int* gx = xs + buf * kStageX + g * SR;
+    int* gs = ss + buf * kStageS + g * (SR + 1);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int m = q * GL + c;
+      const long long e = base + m;
+      if (e < j_hi) cp_async4(gx + m, p.src + e);
+      if (e < t_hi)
+        cp_async4(gs + m, p.seg + e);
+      else
+        gs[m] = -2;
+    }
+    if (c == 0) {
+      const long long e = base + SR;
+      if (e < t_hi)
+        cp_async4(gs + SR, p.seg + e);
+      else
+        gs[SR] = -2;
+    }
+    cp_async_commit();
+  };
 
   float4 acc[NV];
 #pragma unroll
   for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
   float loss_acc = 0.f;
 
+  if (live)
+    stage(j_lo, 0);
+  else
+    cp_async_commit();
+  int buf = 0;
 #pragma unroll 1
-  for (int sr = 0; sr < C; sr += SR) {
+  for (int sr = 0; sr < C; sr += SR, buf ^= 1) {
     const long long base = j_lo + sr;
-    unsigned endm = 0, validm = 0;
+    if (base + SR < j_hi)
+      stage(base + SR, buf ^ 1);
+    else
+      cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int* gx = xs + buf * kStageX + g * SR;
+    const int* gs = ss + buf * kStageS + g * (SR + 1);
+    const int nval = (int)max(0LL, min((long long)SR, j_hi - base));
+    unsigned endm = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const long long e = base + q * GL + c;
-      const bool ok = e < j_hi;
-      int s = -4, sn = -5, x = 0;
-      if (ok) {
-        s = __ldg(p.seg + e);
-        x = __ldg(p.src + e);
-        sn = e + 1 < t_hi ? __ldg(p.seg + e + 1) : -2;
-      }
-      gx[q * GL + c] = x;
-      gs[q * GL + c] = s;
-      const unsigned be = __ballot_sync(0xffffffffu, ok && s != sn);
-      const unsigned bv = __ballot_sync(0xffffffffu, ok);
+      const int m = q * GL + c;
+      const bool end = m < nval && gs[m] != gs[m + 1];
+      const unsigned be = __ballot_sync(0xffffffffu, end);
       endm |= ((be >> (g * GL)) & low_bits<GL>()) << (q * GL);
-      validm |= ((bv >> (g * GL)) & low_bits<GL>()) << (q * GL);
     }
-    __syncwarp();
-    if (__ballot_sync(0xffffffffu, validm != 0) == 0) break;
+    if (__ballot_sync(0xffffffffu, nval > 0) == 0) break;
 #pragma unroll 1
     for (int m0 = 0; m0 < SR; m0 += U) {
+      unsigned ebits = (endm >> m0) & low_bits<U>();
+      // backward: the first segment ending in this batch gets its row state
+      // fetched together with the gathers
+      float4 wpre[FWD ? 1 : NV];
+      float mpre = 0.f;
+      int spre = -7;
+      if constexpr (!FWD) {
+        if (ebits) {
+          spre = gs[m0 + __ffs(ebits) - 1];
+          if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
+        }
+      }
       float4 v[U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int m = m0 + u;
-        const bool ok = (validm >> m) & 1u;
-        const float* row = gbase + (long long)gx[m] * gstride;
+        const bool ok = m0 + u < nval;
+        const float* row = gbase + (size_t)((unsigned)gx[m0 + u]) * gstride;
 #pragma unroll
-        for (int w = 0; w < NV; ++w) {
-          const int cv = c + w * GL;
-          v[u][w] = (ok && cv < nvec) ? ldg4(row + cv * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int w = 0; w < NV; ++w)
+          v[u][w] = (ok && c + w * GL < nvec) ? ldg4(row + w * GL * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      unsigned ebits = (endm >> m0) & low_bits<U>();
       if (ebits == 0) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -217,8 +294,17 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             // completes a segment that began in an earlier chunk -> fixup
             store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
             if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
+          } else if constexpr (FWD) {
+            store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
           } else {
-            finish_segment<FWD, GL, NV>(p, tb, gmask, s, acc, c, loss_acc);
+            if (s == spre) {
+              adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wpre, mpre);
+            } else {
+              float4 wr[NV];
+              float mr;
+              load_row_state<GL, NV>(p, tb, s, c, wr, mr);
+              adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wr, mr);
+            }
           }
 #pragma unroll
           for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -229,6 +315,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     }
     __syncwarp();
   }
+  cp_async_wait<0>();
   // The chunk's last segment continues into the next chunk: hand the partial on.
   if (live && j_hi < t_hi) {
     const int sl = __ldg(p.seg + j_hi - 1);
@@ -246,8 +333,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 
 template <bool FWD>
 __global__ void __launch_bounds__(256, 3) seg_reduce_kernel(SegParams p) {
-  __shared__ int xs[kSegWarps][kStage];
-  __shared__ int ss[kSegWarps][kStage];
+  __shared__ int xs[kSegWarps][2 * kStageX];
+  __shared__ int ss[kSegWarps][2 * kStageS];
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x * kSegWarps + warp;
   if (unit >= p.n_units) return;
