@@ -293,26 +293,19 @@ def main():
     SD = shard.sum_dim
     pooled = shard.pooled_tensor()
 
-    # N>1 plumbing: pooled [B, SD_g] rows of peer p are contiguous -> all_to_all_single
+    # N>1: table-wise shards; pooled rows go to their sample owners and the
+    # gradient comes back with the inverse all-to-all (paper_2208_06399_b200.sharded)
     if world > 1:
-        sds = [0] * world
-        sds[rank] = SD
-        t = torch.tensor(sds, device="cuda", dtype=torch.int64)
-        dist.all_reduce(t)
-        sds = t.tolist()
-        bl = B // world
-        recv = torch.empty(bl * sum(sds), device="cuda", dtype=torch.float32)
-        gback = torch.empty(B * SD, device="cuda", dtype=torch.float32)
-        in_split = [bl * SD] * world
-        out_split = [bl * s for s in sds]
+        from paper_2208_06399_b200.sharded import PooledExchange, a2a_layout
+
+        exch = PooledExchange(a2a_layout(task, plan, B), rank, device="cuda")
 
     def step():
         shard.forward(pooled, stream=stream)
         if world > 1:
-            dist.all_to_all_single(recv, pooled.view(-1), out_split, in_split)
+            recv = exch.forward(pooled)
             # dense part out of scope: loss 1/2|pooled|^2 -> dL/dpooled = pooled (recv)
-            dist.all_to_all_single(gback, recv, in_split, out_split)
-            shard.backward(gback, LR, EPS, stream=stream)
+            shard.backward(exch.backward(recv), LR, EPS, stream=stream)
         else:
             shard.backward(pooled, LR, EPS, stream=stream)
 
@@ -389,7 +382,7 @@ def main():
             shard.load(wl, stream=stream)  # H2D of this step's inputs + on-device validation
             if world > 1:
                 step()
-                loss = torch.dot(recv, recv).mul_(0.5).item()  # step result to host
+                loss = torch.dot(exch.recv_buf, exch.recv_buf).mul_(0.5).item()  # step result to host
             else:
                 loss = shard.step(LR, EPS, want_loss=True, stream=stream)  # D2H of the loss
         barrier()

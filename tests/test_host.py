@@ -1,0 +1,252 @@
+"""Product host library (C++ behind the C-ABI) on CPU: bit-exact generator,
+planners, file formats and error contracts against the golden vectors and the
+oracle; the C-ABI exports every symbol include/autoshard_b200.h declares; the
+device entry points fail loudly (no CPU fallback) without a GPU."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from helpers import to_oracle_tables
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+GOLD = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+
+
+def plan_str(a):
+    return "".join(map(str, a))
+
+
+def cfg1_pool(P):
+    return P.generate_pool(0, 10, P.GeneratorConfig(dim_choices=(64,), pooling_mean_target=20.0))
+
+
+def test_cabi_exports_every_declared_symbol(P):
+    hdr = open(os.path.join(ROOT, "include", "autoshard_b200.h")).read()
+    declared = set(re.findall(r"AS_API\s+[\w\s\*]+?\b(as_\w+)\s*\(", hdr))
+    assert len(declared) >= 40
+    lib = ctypes.CDLL(P.LIB_PATH)
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    from paper_2208_06399_b200._capi import SIGNATURES
+
+    assert declared == set(SIGNATURES), declared ^ set(SIGNATURES)
+    assert P.lib().as_version().decode().startswith("autoshard-b200")
+
+
+def test_generator_cfg1_golden(P, oracle):
+    from oracle import stream_hash
+
+    pool = cfg1_pool(P)
+    assert [vars(t) for t in to_oracle_tables(pool)] == GOLD["cfg1"]["pool"]
+    assert f"{P.fingerprint(pool):016x}" == GOLD["cfg1"]["fingerprint_pool"]
+    wl = P.generate_workload(0, pool, 512)
+    assert f"{stream_hash(oracle.fnv, [(s.offsets, s.indices) for s in wl.per_table]):016x}" == GOLD["cfg1"]["stream_hash"]
+    assert wl.batch_size == 512 and [s.table_id for s in wl.per_table] == [t.id for t in pool]
+
+
+def test_generator_cfg2_golden_parallel(P, oracle):
+    from oracle import stream_hash
+
+    pool = P.generate_pool(0, 856)
+    assert f"{P.fingerprint(pool):016x}" == GOLD["pool856_fingerprint"]
+    p2 = pool[:50]
+    for t in p2:
+        t.dim = 128
+    for threads in (1, 0):
+        wl = P.generate_workload(0, p2, 65536, n_threads=threads)
+        h = stream_hash(oracle.fnv, [(s.offsets, s.indices) for s in wl.per_table])
+        assert f"{h:016x}" == GOLD["cfg2"]["stream_hash"]
+
+
+def test_canonical_serialization_via_files(P, oracle, tmp_path):
+    pool = P.generate_pool(0, 856)
+    wl = P.generate_workload(0, pool[:40], 4096)
+    P.save_pool(str(tmp_path / "p"), pool)
+    wl.save(str(tmp_path / "w"), pool[:40])
+    data = (tmp_path / "p").read_bytes() + (tmp_path / "w").read_bytes()
+    assert f"{oracle.fnv(data):016x}" == GOLD["canonical"]["hash"] and len(data) == GOLD["canonical"]["bytes"]
+    assert P.load_pool(str(tmp_path / "p")) == pool
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_generator_matches_oracle_randomized(P, oracle, seed):
+    rng = np.random.default_rng(100 + seed)
+    kw = dict(hash_size_min=float(rng.choice([1, 7, 1000])), hash_size_max=float(rng.choice([2e3, 3e5])),
+              pooling_mean_target=float(rng.choice([0.0, 1.5, 40.0])), pooling_shape=float(rng.choice([1.5, 2.0, 3.0])),
+              pooling_cap=float(rng.choice([5.0, 193.0])), dim_choices=(16, 32, 48),
+              access_ratio_min=float(rng.choice([1e-3, 0.2, 1.0])))
+    n = int(rng.integers(1, 30))
+    pp = P.generate_pool(seed, n, P.GeneratorConfig(**kw))
+    po = oracle.generate_pool(seed, n, **kw)
+    assert to_oracle_tables(pp) == po
+    B, z = int(rng.integers(1, 500)), float(rng.choice([1.05, 0.5, 1.9]))
+    wl = P.generate_workload(seed, pp, B, z)
+    wo = oracle.generate_workload(seed, po, B, z)
+    for s in wl.per_table:
+        assert np.array_equal(s.offsets, wo[s.table_id][0]) and np.array_equal(s.indices, wo[s.table_id][1])
+
+
+def test_generator_errors(P):
+    with pytest.raises(P.ConfigError):
+        P.generate_pool(0, 4, P.GeneratorConfig(hash_size_min=100.0, hash_size_max=10.0))
+    with pytest.raises(P.ConfigError):
+        P.generate_pool(0, 4, P.GeneratorConfig(dim_choices=()))
+    with pytest.raises(P.ConfigError):
+        P.generate_pool(0, 0)
+    with pytest.raises(P.ConfigError):
+        P.generate_workload(0, [P.TableDesc(id=0, dim=16, hash_size=0, pooling_mean=1.0)], 16)
+    with pytest.raises(P.ConfigError):
+        P.generate_workload(0, [P.TableDesc(id=0, dim=16, hash_size=10)], 0)
+
+
+def test_generator_properties(P):
+    """tests/test_tables.cpp:97-161 invariants, on the product generator."""
+    pool = P.generate_pool(3, 20)
+    wl = P.generate_workload(11, pool, 1024)
+    for t, s in zip(pool, wl.per_table):
+        assert s.table_id == t.id and len(s.offsets) == 1025 and s.offsets[0] == 0
+        assert np.all(np.diff(s.offsets) >= 0) and s.offsets[-1] == len(s.indices)
+        assert len(s.indices) == 0 or (s.indices.min() >= 0 and s.indices.max() < t.hash_size)
+        if t.pooling_mean > 0.5:
+            assert 0.75 * t.pooling_mean <= len(s.indices) / 1024 <= 1.25 * t.pooling_mean
+    z = P.generate_workload(5, [P.TableDesc(id=0, dim=16, hash_size=100, pooling_mean=0.0)], 64)
+    assert len(z.per_table[0].indices) == 0 and not z.per_table[0].offsets.any()
+    one = P.generate_workload(5, [P.TableDesc(id=0, dim=16, hash_size=10, pooling_mean=4.0, access_ratio=0.1)], 256)
+    assert len(set(one.per_table[0].indices.tolist())) == 1
+    sub = pool[4:8]
+    a = P.generate_workload(9, pool[:12], 128)
+    c = P.generate_workload(9, sub, 128)
+    for s in c.per_table:
+        assert np.array_equal(s.indices, a.find(s.table_id).indices)
+
+
+def test_planners_golden_and_errors(P):
+    pool = cfg1_pool(P)
+    task = P.ShardingTask(pool, 2, GOLD["cfg1"]["budget"])
+    K = P.HeuristicKind
+    for kind, key in [(K.kSizeGreedy, "size"), (K.kDimGreedy, "dim"), (K.kLookupGreedy, "lookup")]:
+        assert plan_str(P.greedy_shard(task, kind).assignment) == GOLD["cfg1"]["plans"][key]
+    assert plan_str(P.random_shard(task, 0).assignment) == GOLD["cfg1"]["plans"]["random0"]
+    assert f"{P.fingerprint(task):016x}" == GOLD["cfg1"]["fingerprint_task"]
+    p2 = P.generate_pool(0, 856)[:50]
+    for t in p2:
+        t.dim = 128
+    t2 = P.ShardingTask(p2, 8, GOLD["cfg2"]["budget"])
+    for kind, key in [(K.kSizeGreedy, "size"), (K.kDimGreedy, "dim"), (K.kLookupGreedy, "lookup")]:
+        assert plan_str(P.greedy_shard(t2, kind).assignment) == GOLD["cfg2"]["plans"][key]
+    assert plan_str(P.random_shard(t2, 0).assignment) == GOLD["cfg2"]["plans"]["random0"]
+    with pytest.raises(P.InfeasibleError, match="exceed total budget"):
+        P.greedy_shard(P.ShardingTask(pool, 2, [1, 1]), K.kLookupGreedy)
+    with pytest.raises(P.ConfigError):
+        P.greedy_shard(task, K.kRandom)
+    with pytest.raises(P.ConfigError):
+        P.greedy_shard(P.ShardingTask(pool, 2, [1]), K.kLookupGreedy)
+    spec = [P.TableDesc(id=i, dim=1, hash_size=10, pooling_mean=float(c), bytes_per_param=1)
+            for i, c in enumerate([4, 3, 3, 2, 2])]
+    assert P.greedy_shard(P.ShardingTask(spec, 2, [10 ** 9] * 2), K.kLookupGreedy).assignment == \
+        GOLD["spec_greedy"]["assignment"]
+    assert P.degree_of_balance([0.4, 1.0]) == 0.4 and P.degree_of_balance([0.0, 0.0]) == 1.0
+    with pytest.raises(P.ConfigError):
+        P.degree_of_balance([])
+    assert P.speedup_over([15.0, 3.0], [10.0, 8.0]) == 1.5  # PAPER.md:76 toy
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_planners_match_oracle_randomized(P, oracle, seed):
+    rng = np.random.default_rng(seed)
+    pool = P.generate_pool(seed, int(rng.integers(2, 60)), P.GeneratorConfig(dim_choices=(16, 64, 256)))
+    k = int(rng.integers(1, 9))
+    total = sum(t.size_bytes() for t in pool)
+    budget = [int(total / k * float(rng.choice([1.0, 1.2, 3.0]))) + 1] * k
+    task = P.ShardingTask(pool, k, budget)
+    ot = to_oracle_tables(pool)
+    for kind in range(3):
+        assert P.greedy_shard(task, P.HeuristicKind(kind)).assignment == oracle.greedy_shard(ot, budget, kind)
+    assert P.random_shard(task, seed).assignment == oracle.random_shard(ot, budget, seed)
+
+
+def test_plan_mem_and_file_roundtrip(P, tmp_path):
+    pool = cfg1_pool(P)
+    task = P.ShardingTask(pool, 2, GOLD["cfg1"]["budget"])
+    plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
+    used = plan.mem_used(task)
+    assert sum(used) == task.total_bytes() and plan.feasible(task)
+    assert plan.shard_members(task)[0] == [t.id for t, k in zip(pool, plan.assignment) if k == 0]
+    f = str(tmp_path / "plan.txt")
+    P.save_plan(f, task, plan, [1.5, 2.25])
+    got, costs = P.load_plan(f, task)
+    assert got == plan and costs == [1.5, 2.25]
+    P.save_plan(f, task, plan)
+    assert P.load_plan(f, task) == (plan, None)
+    other = P.ShardingTask(pool, 2, [b + 1 for b in GOLD["cfg1"]["budget"]])
+    with pytest.raises(P.StateError, match="fingerprint"):
+        P.load_plan(f, other)
+    with pytest.raises(P.ConfigError):
+        P.ShardingPlan([0, 5] + [0] * 8).validate(task)
+    with pytest.raises(P.ConfigError):
+        P.ShardingPlan([0]).validate(task)
+
+
+def test_workload_file_reads_reference_file_and_writes_same_bytes(P, tmp_path):
+    g = GOLD["small_workload"]
+    path = os.path.join(HERE, "golden", g["file"])
+    wl, tables = P.load_workload(path)
+    assert [vars(t) for t in to_oracle_tables(tables)] == g["pool"]
+    regen = P.generate_workload(g["seed"], tables, g["batch"])
+    for s in wl.per_table:
+        r = regen.find(s.table_id)
+        assert np.array_equal(s.offsets, r.offsets) and np.array_equal(s.indices, r.indices)
+    out = str(tmp_path / "w")
+    regen.save(out, tables)
+    assert open(out, "rb").read() == open(path, "rb").read()
+
+
+def _corrupt(tmp_path, name, mutate):
+    data = bytearray(open(os.path.join(HERE, "golden", "ref_small.workload"), "rb").read())
+    hdr_end = data.index(b"end_header\n") + len(b"end_header\n")
+    mutate(data, hdr_end)
+    p = tmp_path / name
+    p.write_bytes(bytes(data))
+    return str(p)
+
+
+def test_workload_file_error_contracts(P, tmp_path):
+    """workload_io.hpp:216-241 / tests/test_tables.cpp:327-378."""
+    wl, tables = P.load_workload(os.path.join(HERE, "golden", "ref_small.workload"))
+    t0 = tables[0].id
+
+    def first_offset(d, h):
+        d[h + 8:h + 16] = (7).to_bytes(8, "little", signed=True)
+
+    with pytest.raises(P.OffsetError, match=f"table {t0}: offsets must start at 0, got 7"):
+        P.load_workload(_corrupt(tmp_path, "a", first_offset))
+    n_off = len(wl.per_table[0].offsets)
+
+    def bad_index(d, h):
+        pos = h + 8 + 8 * n_off + 8
+        d[pos:pos + 8] = int(tables[0].hash_size).to_bytes(8, "little", signed=True)
+
+    if len(wl.per_table[0].indices):
+        with pytest.raises(P.IndexError_, match=f"table {t0}: index {tables[0].hash_size} out of range"):
+            P.load_workload(_corrupt(tmp_path, "b", bad_index))
+    with pytest.raises(P.ParseError, match="truncated"):
+        P.load_workload(_corrupt(tmp_path, "c", lambda d, h: d.__delitem__(slice(len(d) - 5, len(d)))))
+    with pytest.raises(P.ParseError, match="bad workload magic"):
+        P.load_workload(_corrupt(tmp_path, "d", lambda d, h: d.__setitem__(slice(0, 4), b"xxxx")))
+    with pytest.raises(P.ParseError):
+        P.load_workload(str(tmp_path / "missing"))
+
+
+def test_device_path_fails_loudly_without_gpu(P):
+    """No CPU fallback: without a visible CUDA device the context cannot be created."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.CudaError):
+        P.EmbeddingShard([P.TableDesc(id=0, dim=16, hash_size=10)], 4)
