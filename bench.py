@@ -348,8 +348,9 @@ def main():
     ms_per_step = t_max / K
     value = B * K / (t_max / 1e3)
 
-    # ---- per-kernel timing pass (events between phases), same stream ----
-    shard.profile(True)
+    # ---- per-kernel timing pass: events around each phase, phases serialized
+    # (the sort's side-stream overlap off) so every kernel is timed alone ----
+    shard.profile(True, serialize=True)
     for i in range(K):
         flush_buf.fill_(float(i))
         step()

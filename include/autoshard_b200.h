@@ -230,8 +230,9 @@ typedef struct as_ctx_info {
 } as_ctx_info;
 AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info);
 
-/* Per-kernel CUDA-event timing for roofline accounting (bench.py). When
- * enabled, every phase of as_forward / as_backward_rowwise_adagrad records an
+/* Per-kernel CUDA-event timing for roofline accounting (bench.py). enable:
+ * 0 off, 1 on, 2 on with the K2 sort serialized into the backward (no
+ * side-stream overlap) so each phase is timed alone. When enabled, every phase of as_forward / as_backward_rowwise_adagrad records an
  * event pair on the launching stream. as_profile_read synchronises and returns
  * the accumulated ms per phase: [0] bag_expand (K4), [1] forward segment
  * reduce (K1), [2] forward fixup, [3] radix sort (K2), [4] backward segment

@@ -1,0 +1,199 @@
+// autoshard_b200.hpp — C++ face of the B200 hot path, shaped like the
+// reference's own interface so it drops into code written against
+// /root/reference/proj/include/autoshard (header-only, over the C-ABI in
+// autoshard_b200.h; link with -lautoshard_b200).
+//
+//   autoshard::measure_plan(plan, task, wl, sim, bench)        simcost.hpp:194
+//     -> autoshard::gpu::measure_plan(plan, task, wl, bench)   measured B200 ms per shard
+//
+// The templates are duck-typed on the reference types (TableDesc, ShardingTask,
+// ShardingPlan, Workload/TableStream, BenchConfig: tables.hpp:24-143,
+// simcost.hpp:163-171), so this header does not include the reference. Define
+// AUTOSHARD_B200_REFERENCE_ERRORS after including "autoshard/common.hpp" to
+// get the reference's exception classes (common.hpp:15-50) instead of
+// autoshard::gpu::Error.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <type_traits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "autoshard_b200.h"
+
+namespace autoshard {
+namespace gpu {
+
+struct Error : std::runtime_error {
+  as_status code;
+  Error(as_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(as_status s, const std::string& msg) {
+#ifdef AUTOSHARD_B200_REFERENCE_ERRORS
+  switch (s) {
+    case AS_CONFIG: throw ::autoshard::ConfigError(msg);
+    case AS_PARSE: throw ::autoshard::ParseError(msg);
+    case AS_OFFSET: throw ::autoshard::OffsetError(msg);
+    case AS_INDEX: throw ::autoshard::IndexError(msg);
+    case AS_INFEASIBLE: throw ::autoshard::InfeasibleError(msg);
+    case AS_SHAPE: throw ::autoshard::ShapeError(msg);
+    case AS_LOOKUP: throw ::autoshard::LookupError(msg);
+    case AS_GUARD: throw ::autoshard::GuardError(msg);
+    case AS_STATE: throw ::autoshard::StateError(msg);
+    default: break;
+  }
+#endif
+  throw Error(s, msg);
+}
+
+[[noreturn]] inline void throw_status(as_status s) { raise(s, as_last_error()); }
+
+inline void check(as_status s) {
+  if (s != AS_OK) throw_status(s);
+}
+
+template <class TableDescT>
+as_table_spec to_spec(const TableDescT& t) {
+  as_table_spec s{};
+  s.id = t.id;
+  s.dim = t.dim;
+  s.hash_size = t.hash_size;
+  s.pooling_mean = t.pooling_mean;
+  s.access_ratio = t.access_ratio;
+  s.bytes_per_param = t.bytes_per_param;
+  return s;
+}
+
+template <class Tables>
+std::vector<as_table_spec> to_specs(const Tables& tables) {
+  std::vector<as_table_spec> v;
+  v.reserve(tables.size());
+  for (const auto& t : tables) v.push_back(to_spec(t));
+  return v;
+}
+
+// Owning handle of an as_workload built from a reference Workload's streams
+// (only the tables listed are copied).
+class WorkloadView {
+ public:
+  template <class WorkloadT, class Tables>
+  WorkloadView(const WorkloadT& wl, const Tables& tables) {
+    std::vector<std::pair<int, const void*>> want;
+    for (const auto& t : tables) {
+      const auto* s = wl.find(t.id);
+      if (!s) throw_missing(t.id);
+      want.push_back({t.id, s});
+    }
+    std::sort(want.begin(), want.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    want.erase(std::unique(want.begin(), want.end(), [](auto& a, auto& b) { return a.first == b.first; }),
+               want.end());
+    std::vector<int32_t> ids;
+    std::vector<const int64_t*> off, idx;
+    std::vector<int64_t> n;
+    using Stream = std::remove_pointer_t<decltype(wl.find(0))>;
+    for (auto& w : want) {
+      const auto* s = static_cast<const Stream*>(w.second);
+      ids.push_back(w.first);
+      off.push_back(s->offsets.data());
+      idx.push_back(s->indices.data());
+      n.push_back(static_cast<int64_t>(s->indices.size()));
+    }
+    as_workload* h = nullptr;
+    check(as_workload_from_arrays(wl.batch_size, static_cast<int32_t>(ids.size()), ids.data(), off.data(),
+                                  idx.data(), n.data(), &h));
+    h_.reset(h);
+  }
+  const as_workload* get() const { return h_.get(); }
+
+ private:
+  [[noreturn]] static void throw_missing(int id) {
+    raise(AS_LOOKUP, "measure_plan: table " + std::to_string(id) + " absent from workload");
+  }
+  struct Del {
+    void operator()(as_workload* w) const { as_workload_destroy(w); }
+  };
+  std::unique_ptr<as_workload, Del> h_;
+};
+
+struct GpuBenchConfig {
+  std::vector<int32_t> devices{0};  // shard k runs on devices[k % size]
+  bool flush_l2 = true;
+  float lr = 0.01f, eps = 1e-8f;
+  uint64_t weight_seed = 0;
+};
+
+// measure_plan (simcost.hpp:194-204) with the simulator replaced by the
+// micro-benchmark of the real kernels: per shard, W warm-up and B measured
+// fwd+bwd steps (L2 flushed before each), trimmed mean of B-2R, in ms.
+template <class Plan, class Task, class WorkloadT, class Bench>
+std::vector<double> measure_plan(const Plan& plan, const Task& task, const WorkloadT& wl, const Bench& bench,
+                                 const GpuBenchConfig& gpu = {}) {
+  const auto specs = to_specs(task.tables);
+  if (plan.assignment.size() != specs.size())
+    raise(AS_CONFIG, "plan: assignment length " + std::to_string(plan.assignment.size()) +
+                         " does not match task table count " + std::to_string(specs.size()));
+  WorkloadView view(wl, task.tables);
+  as_bench_config bc{};
+  bc.warmup = bench.warmup;
+  bc.measure = bench.measure;
+  bc.trim = bench.trim;
+  bc.flush_l2 = gpu.flush_l2 ? 1 : 0;
+  bc.seed = gpu.weight_seed;
+  bc.lr = gpu.lr;
+  bc.eps = gpu.eps;
+  std::vector<int32_t> a(plan.assignment.begin(), plan.assignment.end());
+  std::vector<double> costs(static_cast<size_t>(task.num_shards), 0.0);
+  check(as_measure_plan(specs.data(), static_cast<int32_t>(specs.size()), task.num_shards, a.data(), view.get(),
+                        gpu.devices.data(), static_cast<int32_t>(gpu.devices.size()), &bc, costs.data()));
+  return costs;
+}
+
+// One shard resident on one device (RAII over as_ctx).
+class Shard {
+ public:
+  template <class Tables>
+  Shard(int device, const Tables& tables, int64_t batch, uint64_t weight_seed = 0) {
+    const auto specs = to_specs(tables);
+    as_ctx* c = nullptr;
+    check(as_create(device, specs.data(), static_cast<int32_t>(specs.size()), batch, weight_seed, &c));
+    ctx_.reset(c);
+  }
+  template <class WorkloadT, class Tables>
+  void load(const WorkloadT& wl, const Tables& tables, void* stream = nullptr) {
+    WorkloadView v(wl, tables);
+    check(as_load_workload(ctx_.get(), v.get(), stream));
+  }
+  void forward(float* out = nullptr, void* stream = nullptr) { check(as_forward(ctx_.get(), out, stream)); }
+  void backward(const float* grad, float lr, float eps, void* stream = nullptr) {
+    check(as_backward_rowwise_adagrad(ctx_.get(), grad, lr, eps, stream));
+  }
+  double step(float lr, float eps, void* stream = nullptr) {
+    double loss = 0.0;
+    check(as_step(ctx_.get(), lr, eps, &loss, stream));
+    return loss;
+  }
+  double measure(int warmup, int measure, int trim, bool flush = true, float lr = 0.01f, float eps = 1e-8f) {
+    double ms = 0.0;
+    check(as_measure(ctx_.get(), warmup, measure, trim, flush ? 1 : 0, lr, eps, &ms));
+    return ms;
+  }
+  as_ctx_info info() const {
+    as_ctx_info i{};
+    check(as_ctx_info_get(ctx_.get(), &i));
+    return i;
+  }
+  as_ctx* get() { return ctx_.get(); }
+
+ private:
+  struct Del {
+    void operator()(as_ctx* c) const { as_destroy(c); }
+  };
+  std::unique_ptr<as_ctx, Del> ctx_;
+};
+
+}  // namespace gpu
+}  // namespace autoshard

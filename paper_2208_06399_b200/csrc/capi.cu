@@ -401,7 +401,7 @@ AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info) {
 AS_API as_status as_profile_enable(as_ctx* ctx, int32_t enable) {
   return guard([&] {
     need(ctx, "ctx");
-    ctx->impl->profile_enable(enable != 0);
+    ctx->impl->profile_enable(enable);
   });
 }
 

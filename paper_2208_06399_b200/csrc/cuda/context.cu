@@ -124,7 +124,10 @@ struct EmbContext::Phase {
   }
 };
 
-void EmbContext::profile_enable(bool on) { prof_ = on; }
+void EmbContext::profile_enable(int mode) {
+  prof_ = mode != 0;
+  prof_serial_ = mode == 2;
+}
 
 void EmbContext::profile_read(double* ms, int64_t* launches, bool reset) {
   DeviceGuard g(device_);
@@ -417,11 +420,13 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
     ++launches_;
   }
   if (n_chunks_ == 0) return;
-  cuda_check(cudaEventRecord(ev_fork_, s), "fork");
-  cuda_check(cudaStreamWaitEvent(side_, ev_fork_, 0), "fork wait");
-  launch_sort(side_);
-  cuda_check(cudaEventRecord(ev_join_, side_), "join");
-  sort_pending_ = true;
+  if (!prof_serial_) {
+    cuda_check(cudaEventRecord(ev_fork_, s), "fork");
+    cuda_check(cudaStreamWaitEvent(side_, ev_fork_, 0), "fork wait");
+    launch_sort(side_);
+    cuda_check(cudaEventRecord(ev_join_, side_), "join");
+    sort_pending_ = true;
+  }
   SegParams p = seg_params(true);
   p.W_ro = W_;
   p.out = target;

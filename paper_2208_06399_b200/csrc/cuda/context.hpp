@@ -37,7 +37,7 @@ class EmbContext {
   // Per-phase CUDA-event timing (bag_expand, fwd_seg, fwd_fixup, sort,
   // bwd_seg, bwd_fixup) and launch counting, for bench.py's roofline.
   static constexpr int kPhases = 6;
-  void profile_enable(bool on);
+  void profile_enable(int mode);  // 0 off, 1 on, 2 on + serialized (no side-stream sort)
   void profile_read(double* ms, int64_t* launches, bool reset);
 
   int device() const { return device_; }
@@ -100,6 +100,7 @@ class EmbContext {
   int64_t bytes_ = 0;
   int64_t launches_ = 0;
   bool prof_ = false;
+  bool prof_serial_ = false;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used_;
   cudaEvent_t ev_get();

@@ -126,8 +126,9 @@ class EmbeddingShard:
     # -- profiling ---------------------------------------------------------
     PHASES = ("bag_expand", "fwd_segreduce", "fwd_fixup", "radix_sort", "bwd_segreduce_adagrad", "bwd_fixup")
 
-    def profile(self, enable: bool = True) -> None:
-        check(lib().as_profile_enable(self._h, int(enable)))
+    def profile(self, enable: bool = True, serialize: bool = False) -> None:
+        """Per-phase event timing; serialize=True runs the sort inside the backward (no overlap)."""
+        check(lib().as_profile_enable(self._h, (2 if serialize else 1) if enable else 0))
 
     def profile_read(self, reset: bool = True):
         """-> ({phase: ms accumulated}, kernel launches) since the last reset."""

@@ -250,3 +250,16 @@ def test_device_path_fails_loudly_without_gpu(P):
         pytest.skip("GPU present")
     with pytest.raises(P.CudaError):
         P.EmbeddingShard([P.TableDesc(id=0, dim=16, hash_size=10)], 4)
+
+
+def test_cpp_dropin_example_against_reference_types(P):
+    """tests/cpp/dropin_example.cpp: reference C++ types -> autoshard::gpu::measure_plan.
+    Built only where the reference headers were mounted at build time."""
+    import subprocess
+
+    exe = os.path.join(HERE, "cpp", "dropin_example")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in example not built (reference headers absent at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sim  ms:" in r.stdout and "gpu  " in r.stdout
