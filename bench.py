@@ -43,6 +43,14 @@ def build_workload(P, name):
         for t in tables:
             t.dim = 128
         return tables, 65536, "cfg2: generate_pool(0,856)[0:50], dim:=128, batch 65536, zipf 1.05"
+    if name == "cfg2u":
+        # SURVEY.md §8d uniform-access control: cfg2 with access_ratio = 1 and
+        # zipf ~ 0, so gathered rows are nearly all distinct (DRAM-bound)
+        tables = P.generate_pool(0, 856)[:50]
+        for t in tables:
+            t.dim = 128
+            t.access_ratio = 1.0
+        return tables, 65536, "cfg2u: cfg2 with access_ratio=1, zipf 1e-6 (uniform-access control)"
     if name == "cfg3":
         tables = P.generate_pool(0, 100, P.GeneratorConfig(dim_choices=(32, 64, 128, 256)))
         return tables, 65536, "cfg3: generate_pool(0,100,dims {32,64,128,256}), batch 65536"
@@ -246,7 +254,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="auto", help="cfg1|cfg2|cfg3|cfg4 (auto: cfg2 at N=1, cfg4 at N>1)")
+    ap.add_argument("--workload", default="auto",
+                    help="cfg1|cfg2|cfg2u|cfg3|cfg4 (auto: cfg2 at N=1, cfg4 at N>1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
@@ -284,7 +293,8 @@ def main():
         plan_name = "single shard"
         mine = list(tables_all)
 
-    wl = P.generate_workload(0, mine, B)  # subset-stable: identical to the full-pool streams
+    zipf = 1e-6 if wname == "cfg2u" else 1.05
+    wl = P.generate_workload(0, mine, B, zipf)  # subset-stable: identical to the full-pool streams
     wl.pin()
     L, U = stream_stats(wl, mine)
     shard = P.EmbeddingShard(mine, B, device=local, weight_seed=WEIGHT_SEED)
