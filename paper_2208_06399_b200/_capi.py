@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libautoshard_b200.so")
+LIB_PATH = os.environ.get("AUTOSHARD_B200_LIB") or os.path.join(HERE, "libautoshard_b200.so")
 
 
 class TableSpecC(C.Structure):

@@ -13,7 +13,7 @@
 #include "context.hpp"
 #include "kernels.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
+#include "sort.cuh"
 
 #include <algorithm>
 #include <cstring>
@@ -269,9 +269,8 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
     sbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     stage_idx_ = static_cast<long long*>(dalloc(sizeof(long long) * cap));
     size_t tmp = 0;
-    cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(nullptr, tmp, (const unsigned*)nullptr, (unsigned*)nullptr,
-                                               (const int*)nullptr, (int*)nullptr, (int)cap, 0, end_bit_),
-               "cub sizing");
+    cuda_check(sort_pairs(nullptr, tmp, nullptr, nullptr, nullptr, nullptr, (int)cap, end_bit_, nullptr),
+               "sort sizing");
     cub_bytes_ = tmp;
     cub_tmp_ = dalloc(tmp);
     cap_L_ = cap;
@@ -455,12 +454,11 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
 void EmbContext::launch_sort(cudaStream_t s) {
   size_t tmp = cub_bytes_;
   Phase ph(this, 3, s);
-  cuda_check(CUB_NS_QUALIFIER::DeviceRadixSort::SortPairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_),
-                                                          reinterpret_cast<unsigned*>(skey_), bag_, sbag_, (int)L_, 0,
-                                                          end_bit_, s),
-             "cub SortPairs");
-  // onesweep: histogram + exclusive-sum + one pass per 8 key bits
-  launches_ += 2 + (end_bit_ + 7) / 8;
+  cuda_check(sort_pairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_), reinterpret_cast<unsigned*>(skey_),
+                        bag_, sbag_, (int)L_, end_bit_, s),
+             "radix sort");
+  // onesweep: histogram + exclusive-sum + one pass per digit
+  launches_ += 2 + sort_passes(end_bit_);
 }
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
@@ -617,7 +615,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + (end_bit_ + 7) / 8);
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + sort_passes(end_bit_));
 }
 
 }  // namespace asb

@@ -160,6 +160,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // SASS, fits the instruction cache). The backward prefetches the weight row
 // and momentum of the first segment ending in a batch together with the
 // batch's gradient gathers.
+#ifndef ASB_GATHER_U
+#define ASB_GATHER_U 4
+#endif
 constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
 constexpr int kStageX = 256;  // staged row ids per warp per buffer (R * SR)
 constexpr int kStageS = 288;  // staged keys per warp per buffer (R * (SR + 1))
@@ -169,7 +172,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
   constexpr int Q = SR / GL;                       // elements staged per lane per super-round
-  constexpr int U = NV >= 8 ? 1 : 8 / NV;          // gathers in flight per lane
+  constexpr int U = NV >= ASB_GATHER_U ? 1 : ASB_GATHER_U / NV;  // gathers in flight per lane
   static_assert(R * SR <= kStageX && R * (SR + 1) <= kStageS, "stage too small");
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
@@ -332,7 +335,10 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 }
 
 template <bool FWD>
-__global__ void __launch_bounds__(256, 3) seg_reduce_kernel(SegParams p) {
+#ifndef ASB_SEG_MINBLOCKS
+#define ASB_SEG_MINBLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegParams p) {
   __shared__ int xs[kSegWarps][2 * kStageX];
   __shared__ int ss[kSegWarps][2 * kStageS];
   const int warp = threadIdx.x >> 5;
