@@ -379,29 +379,43 @@ def main():
                 "ms_per_launch": round(dom_ms, 4)}
     step_gbs = (fwd_b + bwd_b) / (ms_per_step / 1e3) / 1e9
 
-    # ---- e2e through the public API: pinned host int64 streams -> device each step ----
+    # ---- e2e through the public API: every step's int64 streams go host (pinned)
+    # -> device. Pipelined like a training loop: batch i+1 is staged (H2D on the
+    # copy engine) while batch i computes; commit = on-device pack + validation;
+    # the loss of each step is read back (D2H) and the batch's validation checked ----
     e2e = None
     if not args.no_e2e and not args.profile_only:
         h2d = sum(8 * (B + 1) + 8 * l for l in L) + 40 * len(mine)
         d2h = 8 + 8
-        for _ in range(2):
-            shard.load(wl, stream=stream)
-            shard.step(LR, EPS, want_loss=True, stream=stream)
+
+        def e2e_step():
+            if world > 1:
+                step()
+                return torch.dot(exch.recv_buf, exch.recv_buf).mul_(0.5).item()
+            return shard.step(LR, EPS, want_loss=True, stream=stream)
+
+        shard.stage(wl)
+        shard.commit(stream)
+        for _ in range(2):  # warm-up of the pipelined loop
+            shard.stage(wl)
+            e2e_step()
+            shard.commit(stream)
+        shard.stage(wl)
         barrier()
         t0 = time.perf_counter()
         for i in range(K):
-            shard.load(wl, stream=stream)  # H2D of this step's inputs + on-device validation
-            if world > 1:
-                step()
-                loss = torch.dot(exch.recv_buf, exch.recv_buf).mul_(0.5).item()  # step result to host
-            else:
-                loss = shard.step(LR, EPS, want_loss=True, stream=stream)  # D2H of the loss
+            loss = e2e_step()  # batch i (its H2D overlapped the previous step)
+            shard.commit(stream)  # batch i+1 becomes current (waits for its copy)
+            shard.stage(wl)  # batch i+2 -> copy engine, overlaps the next step
+        shard.commit(stream)
+        shard.check()  # drain: every copy issued in the region has landed
         barrier()
         te = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(B * K / float(te.item()), 1), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": d2h, "ms_per_step": round(float(te.item()) * 1e3 / K, 3),
+               "pipelined": "H2D of batch i+1 overlaps compute of batch i (as_stage_workload / as_commit_staged)",
                "loss_last": loss}
 
     cpu = None

@@ -180,6 +180,22 @@ AS_API as_status as_load_streams(as_ctx* ctx, const int64_t* const* offsets,
 /* Same, picking the ctx's tables from a workload by id (LookupError if absent). */
 AS_API as_status as_load_workload(as_ctx* ctx, const as_workload* wl, void* stream);
 
+/* Asynchronous, double-buffered loading for training loops: stage batch i+1
+ * (host->device copy on the context's copy stream; returns without waiting
+ * when the host buffers are pinned — they must stay valid until the copy
+ * completes, i.e. until the matching as_commit_staged has been issued and the
+ * stream reached it) while batch i computes, then commit it. as_commit_staged
+ * packs + validates on `stream` (async) and makes it the current batch;
+ * its OffsetError / IndexError is reported by as_check_batch, or by the next
+ * synchronising call (as_step with a loss, as_measure, readbacks). Two slots:
+ * staging a third batch before a commit returns AS_STATE. as_load_streams is
+ * stage + commit + check. */
+AS_API as_status as_stage_streams(as_ctx* ctx, const int64_t* const* offsets,
+                                  const int64_t* const* indices, const int64_t* n_indices);
+AS_API as_status as_stage_workload(as_ctx* ctx, const as_workload* wl);
+AS_API as_status as_commit_staged(as_ctx* ctx, void* stream);
+AS_API as_status as_check_batch(as_ctx* ctx);
+
 /* K4+K1: pooled[b, col_t + d] = sum_{j in bag (t,b)} W_t[idx_j, d]; empty bag -> 0.
  * out: device [batch, sum_dim] fp32, or NULL for the ctx's own buffer. */
 AS_API as_status as_forward(as_ctx* ctx, float* out_or_null, void* stream);

@@ -106,6 +106,10 @@ SIGNATURES = {
     "as_destroy": (i32, [vp]),
     "as_load_streams": (i32, [vp, P(vp), P(vp), P(i64), vp]),
     "as_load_workload": (i32, [vp, vp, vp]),
+    "as_stage_streams": (i32, [vp, P(vp), P(vp), P(i64)]),
+    "as_stage_workload": (i32, [vp, vp]),
+    "as_commit_staged": (i32, [vp, vp]),
+    "as_check_batch": (i32, [vp]),
     "as_forward": (i32, [vp, vp, vp]),
     "as_backward_rowwise_adagrad": (i32, [vp, vp, f32, f32, vp]),
     "as_step": (i32, [vp, f32, f32, P(f64), vp]),

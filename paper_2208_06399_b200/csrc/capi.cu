@@ -61,6 +61,32 @@ asb::GenConfig to_cfg(const as_generator_config* c) {
 
 const int32_t kDefaultDims[2] = {16, 32};
 
+// Per-table stream pointers of ctx's tables, picked from a workload by id.
+struct Picked {
+  std::vector<const int64_t*> off, idx;
+  std::vector<int64_t> n;
+};
+Picked pick_streams(asb::EmbContext& ctx, const asb::HostWorkload& wl) {
+  const int T = ctx.n_tables();
+  Picked p;
+  p.off.resize(static_cast<size_t>(T));
+  p.idx.resize(static_cast<size_t>(T));
+  p.n.resize(static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t) {
+    const int pos = wl.find(ctx.spec(t).id);
+    if (pos < 0)
+      asb::fail(AS_LOOKUP, "measure: table " + std::to_string(ctx.spec(t).id) + " absent from workload");
+    const auto& st = wl.per_table[static_cast<size_t>(pos)];
+    if (static_cast<int64_t>(st.offsets.size()) != wl.batch_size + 1)
+      asb::fail(AS_OFFSET, "table " + std::to_string(st.table_id) + ": offsets length " +
+                               std::to_string(st.offsets.size()) + " != batch_size + 1");
+    p.off[t] = st.offsets.data();
+    p.idx[t] = st.indices.data();
+    p.n[t] = static_cast<int64_t>(st.indices.size());
+  }
+  return p;
+}
+
 void load_from_workload(asb::EmbContext& ctx, const asb::HostWorkload& wl, cudaStream_t s) {
   const int T = ctx.n_tables();
   std::vector<const int64_t*> off(static_cast<size_t>(T)), idx(static_cast<size_t>(T));
@@ -328,6 +354,42 @@ AS_API as_status as_load_workload(as_ctx* ctx, const as_workload* wl, void* stre
     need(ctx, "ctx");
     need(wl, "wl");
     load_from_workload(*ctx->impl, wl->wl, static_cast<cudaStream_t>(stream));
+  });
+}
+
+AS_API as_status as_stage_streams(as_ctx* ctx, const int64_t* const* offsets, const int64_t* const* indices,
+                                  const int64_t* n_indices) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (ctx->impl->n_tables() > 0) {
+      need(offsets, "offsets");
+      need(indices, "indices");
+      need(n_indices, "n_indices");
+    }
+    ctx->impl->stage(offsets, indices, n_indices);
+  });
+}
+
+AS_API as_status as_stage_workload(as_ctx* ctx, const as_workload* wl) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(wl, "wl");
+    Picked p = pick_streams(*ctx->impl, wl->wl);
+    ctx->impl->stage(p.off.data(), p.idx.data(), p.n.data());
+  });
+}
+
+AS_API as_status as_commit_staged(as_ctx* ctx, void* stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->impl->commit(static_cast<cudaStream_t>(stream));
+  });
+}
+
+AS_API as_status as_check_batch(as_ctx* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->impl->check();
   });
 }
 

@@ -16,6 +16,7 @@
 #include "sort.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 namespace asb {
@@ -192,6 +193,11 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     max_dim_ = std::max(max_dim_, s.dim);
   }
   total_w_ = w_off;
+  for (int t = 0; t < n; ++t) {
+    stage_x_ = std::max(stage_x_, stage_x_ints(htabs_[t].kind));
+    stage_s_ = std::max(stage_s_, stage_s_ints(htabs_[t].kind));
+  }
+  seg_smem_bytes_ = static_cast<size_t>(kSegWarps) * 2 * (stage_x_ + stage_s_) * sizeof(int);
   if (total_rows_ >= (1LL << 31))
     fail(AS_SHAPE, "as_create: a shard holds at most 2^31-1 rows (int32 row ids), got " +
                        std::to_string(total_rows_));
@@ -203,7 +209,14 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   M_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_rows_)));
   out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
   off32_ = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
-  stage_off_ = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
+  for (Slot& sl : slots_) {
+    sl.off64 = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
+    cuda_check(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming), "event");
+  }
+  cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+  cuda_check(cudaMallocHost(&err_host_, sizeof(unsigned long long)), "pinned err word");
+  *err_host_ = ~0ull;
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
   counters_ = static_cast<int*>(dalloc(sizeof(int) * 4));
@@ -216,6 +229,16 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
   flush_ = dalloc(flush_bytes_);
 
+  // Index staging is small: carve out just enough shared memory for the
+  // resident CTAs and leave the rest of the unified 228 KB to L1 (hot rows).
+  {
+    const double need = (double)ASB_SEG_MINBLOCKS * (double)(seg_smem_bytes_ + 1024);
+    const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)) + 1);
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
+               "carveout");
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
+               "carveout");
+  }
   cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
@@ -247,6 +270,12 @@ EmbContext::~EmbContext() {
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
+  if (copy_) cudaStreamDestroy(copy_);
+  for (Slot& sl : slots_) {
+    if (sl.copied) cudaEventDestroy(sl.copied);
+    if (sl.consumed) cudaEventDestroy(sl.consumed);
+  }
+  if (err_host_) cudaFreeHost(err_host_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (prev >= 0) cudaSetDevice(prev);
@@ -261,13 +290,12 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   };
   if (L > cap_L_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
-    for (void* p : {(void*)idx32_, (void*)bag_, (void*)skey_, (void*)sbag_, (void*)stage_idx_, cub_tmp_}) drop(p);
+    for (void* p : {(void*)idx32_, (void*)bag_, (void*)skey_, (void*)sbag_, cub_tmp_}) drop(p);
     const int64_t cap = std::max<int64_t>(L + L / 8, 1024);
     idx32_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     bag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     skey_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     sbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
-    stage_idx_ = static_cast<long long*>(dalloc(sizeof(long long) * cap));
     size_t tmp = 0;
     cuda_check(sort_pairs(nullptr, tmp, nullptr, nullptr, nullptr, nullptr, (int)cap, end_bit_, nullptr),
                "sort sizing");
@@ -295,24 +323,23 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   }
 }
 
-void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
-                      cudaStream_t s) {
+// ---- batch loading: stage (async H2D into one of two slots) -> commit
+// (pack + validate into the working arrays on the compute stream) -> check.
+void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx) {
   DeviceGuard g(device_);
-  loaded_ = false;
-  if (sort_pending_) {  // a forward's side-stream sort may still read the old batch
-    cuda_check(cudaStreamSynchronize(side_), "side sync");
-    sort_pending_ = false;
-  }
+  Slot& sl = slots_[next_stage_];
+  if (sl.staged) fail(AS_STATE, "as_stage_streams: both staging slots hold uncommitted batches");
   // Chunk length: ~128 KB of gathered rows per group, shrunk for small
   // batches so that there is at least about one wave of warps.
   double gbytes = 0.0;
   for (int t = 0; t < T_; ++t) gbytes += 4.0 * specs_[t].dim * (double)std::max<int64_t>(n_idx[t], 0);
   const double target = std::max(2048.0, std::min(131072.0, gbytes / (148.0 * 24.0)));
-  for (int t = 0; t < T_; ++t) htabs_[t].chunk_len = chunk_len_for(specs_[t].dim, target);
+  sl.tabs = htabs_;
   int64_t L = 0, nch = 0, nun = 0;
   for (int t = 0; t < T_; ++t) {
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
-    DevTable& d = htabs_[t];
+    DevTable& d = sl.tabs[t];
+    d.chunk_len = chunk_len_for(specs_[t].dim, target);
     const int R = 32 >> std::min(d.kind, 5);
     const int64_t chunks = (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
     const int64_t units = (chunks + R - 1) / R;
@@ -327,61 +354,121 @@ void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indic
   }
   if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
   if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
-  ensure_capacity(L, nch, nun);
-  std::vector<int> utab(static_cast<size_t>(nun));
+  sl.L = L;
+  sl.nch = nch;
+  sl.nun = nun;
+  sl.utab.assign(static_cast<size_t>(nun), 0);
   for (int t = 0; t < T_; ++t)
-    std::fill(utab.begin() + htabs_[t].unit_off, utab.begin() + htabs_[t].unit_off + htabs_[t].n_units, t);
-  // H2D: raw int64 CSR into staging (pinned sources run at full PCIe rate).
+    std::fill(sl.utab.begin() + sl.tabs[t].unit_off, sl.utab.begin() + sl.tabs[t].unit_off + sl.tabs[t].n_units, t);
+  if (L > sl.cap) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    if (sl.idx64) {
+      auto it = std::find(allocs_.begin(), allocs_.end(), (void*)sl.idx64);
+      if (it != allocs_.end()) allocs_.erase(it);
+      cudaFree(sl.idx64);
+    }
+    sl.cap = std::max<int64_t>(L + L / 8, 1024);
+    sl.idx64 = static_cast<long long*>(dalloc(sizeof(long long) * sl.cap));
+  }
+  // the previous commit from this slot must have finished reading it
+  cuda_check(cudaStreamWaitEvent(copy_, sl.consumed, 0), "slot reuse");
+  // H2D: raw int64 CSR (pinned sources run at full PCIe rate on the copy engine)
   for (int t = 0; t < T_; ++t) {
-    cuda_check(cudaMemcpyAsync(stage_off_ + (int64_t)t * (B_ + 1), offsets[t], sizeof(int64_t) * (B_ + 1),
-                               cudaMemcpyHostToDevice, s),
+    cuda_check(cudaMemcpyAsync(sl.off64 + (int64_t)t * (B_ + 1), offsets[t], sizeof(int64_t) * (B_ + 1),
+                               cudaMemcpyHostToDevice, copy_),
                "offsets H2D");
     if (n_idx[t] > 0)
-      cuda_check(cudaMemcpyAsync(stage_idx_ + htabs_[t].idx_off, indices[t], sizeof(int64_t) * n_idx[t],
-                                 cudaMemcpyHostToDevice, s),
+      cuda_check(cudaMemcpyAsync(sl.idx64 + sl.tabs[t].idx_off, indices[t], sizeof(int64_t) * n_idx[t],
+                                 cudaMemcpyHostToDevice, copy_),
                  "indices H2D");
   }
+  cuda_check(cudaEventRecord(sl.copied, copy_), "copied");
+  sl.staged = true;
+  next_stage_ ^= 1;
+}
+
+void EmbContext::commit(cudaStream_t s) {
+  DeviceGuard g(device_);
+  Slot& sl = slots_[next_commit_];
+  if (!sl.staged) fail(AS_STATE, "as_commit_staged: no staged batch");
+  loaded_ = false;
+  if (sort_pending_) {  // a forward's side-stream sort still reads the previous batch
+    cuda_check(cudaStreamWaitEvent(s, ev_join_, 0), "join sort");
+    sort_pending_ = false;
+  }
+  if (sl.L > cap_L_ || sl.nch > cap_chunks_ || sl.nun > cap_units_)
+    cuda_check(cudaStreamSynchronize(s), "grow sync");
+  ensure_capacity(sl.L, sl.nch, sl.nun);
+  cuda_check(cudaStreamWaitEvent(s, sl.copied, 0), "wait copy");
+  htabs_ = sl.tabs;
   if (T_ > 0)
     cuda_check(cudaMemcpyAsync(dtabs_, htabs_.data(), sizeof(DevTable) * T_, cudaMemcpyHostToDevice, s),
                "tables H2D");
-  if (nun > 0)
-    cuda_check(cudaMemcpyAsync(unit_table_, utab.data(), sizeof(int) * nun, cudaMemcpyHostToDevice, s),
+  if (sl.nun > 0)
+    cuda_check(cudaMemcpyAsync(unit_table_, sl.utab.data(), sizeof(int) * sl.nun, cudaMemcpyHostToDevice, s),
                "unit table H2D");
   cuda_check(cudaMemsetAsync(err_, 0xff, sizeof(unsigned long long), s), "err reset");
   if (T_ > 0) {
     const long long n = (long long)T_ * (B_ + 1);
     pack_offsets_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, s>>>(
-        stage_off_, T_, (int)B_, dtabs_, off32_, err_);
+        sl.off64, T_, (int)B_, dtabs_, off32_, err_);
     cuda_check(cudaGetLastError(), "pack_offsets_kernel");
   }
-  if (nun > 0) {
-    pack_indices_kernel<<<grid_for(nun, kWarpsPerBlock), kBlock, 0, s>>>(stage_idx_, dtabs_, unit_table_,
-                                                                        (int)nun, idx32_, err_);
+  if (sl.nun > 0) {
+    pack_indices_kernel<<<grid_for(sl.nun, kWarpsPerBlock), kBlock, 0, s>>>(sl.idx64, dtabs_, unit_table_,
+                                                                           (int)sl.nun, idx32_, err_);
     cuda_check(cudaGetLastError(), "pack_indices_kernel");
   }
-  unsigned long long err = 0;
-  cuda_check(cudaMemcpyAsync(&err, err_, sizeof err, cudaMemcpyDeviceToHost, s), "err D2H");
-  cuda_check(cudaStreamSynchronize(s), "load sync");
-  if (err != ~0ull) {
-    const int t = static_cast<int>(err >> 42);
-    const int kind = static_cast<int>((err >> 40) & 3);
-    const int64_t q = static_cast<int64_t>(err & ((1ull << 40) - 1));
-    const std::string where = "table " + std::to_string(specs_[t].id);
-    switch (kind) {
-      case 0: fail(AS_OFFSET, where + ": offsets must start at 0, got " + std::to_string(offsets[t][0]));
-      case 1: fail(AS_OFFSET, where + ": offsets must be nondecreasing at entry " + std::to_string(q));
-      case 2:
-        fail(AS_OFFSET, where + ": final offset " + std::to_string(offsets[t][B_]) + " != index count " +
-                            std::to_string(n_idx[t]));
-      default:
-        fail(AS_INDEX, where + ": index " + std::to_string(indices[t][q]) + " out of range [0, " +
-                           std::to_string(specs_[t].hash_size) + ")");
-    }
-  }
-  L_ = L;
-  n_chunks_ = nch;
-  n_units_ = nun;
+  cuda_check(cudaMemcpyAsync(err_host_, err_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "err D2H");
+  cuda_check(cudaEventRecord(sl.consumed, s), "consumed");
+  L_ = sl.L;
+  n_chunks_ = sl.nch;
+  n_units_ = sl.nun;
   loaded_ = true;
+  check_pending_ = true;
+  check_slot_ = next_commit_;
+  sl.staged = false;
+  next_commit_ ^= 1;
+}
+
+// Reports the validation result of the last commit (synchronises on it).
+void EmbContext::check() {
+  if (!check_pending_) return;
+  DeviceGuard g(device_);
+  const Slot& sl = slots_[check_slot_];
+  cuda_check(cudaEventSynchronize(sl.consumed), "load sync");
+  check_pending_ = false;
+  const unsigned long long err = *err_host_;
+  if (err == ~0ull) return;
+  loaded_ = false;
+  const int t = static_cast<int>(err >> 42);
+  const int kind = static_cast<int>((err >> 40) & 3);
+  const int64_t q = static_cast<int64_t>(err & ((1ull << 40) - 1));
+  const std::string where = "table " + std::to_string(specs_[t].id);
+  // the offending value is read back from the slot's staging copy
+  auto staged = [&](const long long* p) {
+    long long v = 0;
+    cuda_check(cudaMemcpy(&v, p, sizeof v, cudaMemcpyDeviceToHost), "err value D2H");
+    return v;
+  };
+  switch (kind) {
+    case 0:
+      fail(AS_OFFSET, where + ": offsets must start at 0, got " + std::to_string(staged(sl.off64 + (int64_t)t * (B_ + 1))));
+    case 1: fail(AS_OFFSET, where + ": offsets must be nondecreasing at entry " + std::to_string(q));
+    case 2:
+      fail(AS_OFFSET, where + ": final offset " + std::to_string(staged(sl.off64 + (int64_t)t * (B_ + 1) + B_)) +
+                          " != index count " + std::to_string(sl.tabs[t].n_lookups));
+    default:
+      fail(AS_INDEX, where + ": index " + std::to_string(staged(sl.idx64 + sl.tabs[t].idx_off + q)) +
+                         " out of range [0, " + std::to_string(specs_[t].hash_size) + ")");
+  }
+}
+
+void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
+                      cudaStream_t s) {
+  stage(offsets, indices, n_idx);
+  commit(s);
+  check();
 }
 
 void EmbContext::require_loaded(const char* what) const {
@@ -402,6 +489,8 @@ SegParams EmbContext::seg_params(bool fwd) const {
   p.src = fwd ? idx32_ : sbag_;
   p.carry = carry_;
   p.carry_stride = max_dim_;
+  p.stage_x = stage_x_;
+  p.stage_s = stage_s_;
   return p;
 }
 
@@ -435,7 +524,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 1, s);
-    seg_reduce_kernel<true><<<grid, kBlock, 0, s>>>(p);
+    seg_reduce_kernel<true><<<grid, kBlock, seg_smem_bytes_, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_reduce_kernel<fwd>");
   }
   {
@@ -482,7 +571,7 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   cuda_check(cudaMemsetAsync(counters_ + 2, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 4, s);
-    seg_reduce_kernel<false><<<grid, kBlock, 0, s>>>(p);
+    seg_reduce_kernel<false><<<grid, kBlock, seg_smem_bytes_, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_reduce_kernel<bwd>");
   }
   {
@@ -503,6 +592,7 @@ void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
   if (loss_host) {
     cuda_check(cudaMemcpyAsync(loss_host, loss_, sizeof(double), cudaMemcpyDeviceToHost, s), "loss D2H");
     cuda_check(cudaStreamSynchronize(s), "step sync");
+    check();  // report a bad batch with the step's result
   }
 }
 
@@ -510,6 +600,7 @@ double EmbContext::measure(int warmup, int measure, int trim, bool flush, float 
   if (warmup < 0 || measure < 1 || trim < 0 || measure - 2 * trim < 1)
     fail(AS_CONFIG, "micro_benchmark: need measure - 2*trim >= 1, got B=" + std::to_string(measure) +
                         " R=" + std::to_string(trim));
+  check();
   require_loaded("as_measure");
   DeviceGuard g(device_);
   cudaStream_t s;
@@ -539,6 +630,7 @@ double EmbContext::measure(int warmup, int measure, int trim, bool flush, float 
 }
 
 void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
+  check();
   if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_read_rows: table position " + std::to_string(t) + " out of range");
   for (int64_t i = 0; i < n; ++i)
     if (rows[i] < 0 || rows[i] >= specs_[t].hash_size)
@@ -559,6 +651,7 @@ void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
 }
 
 void EmbContext::read_momentum(int t, const int64_t* rows, int64_t n, float* out) {
+  check();
   if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_read_momentum: table position out of range");
   if (n == 0) return;
   DeviceGuard g(device_);
@@ -572,6 +665,7 @@ void EmbContext::read_momentum(int t, const int64_t* rows, int64_t n, float* out
 }
 
 void EmbContext::read_buffer(int what, void* host, int64_t nbytes) {
+  check();
   DeviceGuard g(device_);
   const void* src = nullptr;
   int64_t want = 0;

@@ -23,6 +23,11 @@ class EmbContext {
 
   void load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
             cudaStream_t s);
+  // asynchronous double-buffered loading: stage (H2D on the copy stream),
+  // commit (pack + validate on s), check (sync + report errors)
+  void stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx);
+  void commit(cudaStream_t s);
+  void check();
   void forward(float* out, double* loss_dev, cudaStream_t s);
   void backward(const float* grad, float lr, float eps, cudaStream_t s);
   void step(float lr, float eps, double* loss_host, cudaStream_t s);
@@ -59,6 +64,8 @@ class EmbContext {
   std::vector<DevTable> htabs_;
   int64_t sum_dim_ = 0, total_rows_ = 0, total_w_ = 0;
   int max_dim_ = 4;
+  int stage_x_ = 32, stage_s_ = 33;
+  size_t seg_smem_bytes_ = 0;
   int end_bit_ = 1;
 
   DevTable* dtabs_ = nullptr;
@@ -66,7 +73,21 @@ class EmbContext {
   float* M_ = nullptr;
   float* out_ = nullptr;
   int* off32_ = nullptr;
-  long long* stage_off_ = nullptr;
+  struct Slot {
+    long long* off64 = nullptr;  // [T*(B+1)] staged int64 offsets
+    long long* idx64 = nullptr;  // [cap] staged int64 indices
+    int64_t cap = 0;
+    std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
+    std::vector<int> utab;
+    int64_t L = 0, nch = 0, nun = 0;
+    cudaEvent_t copied = nullptr, consumed = nullptr;
+    bool staged = false;
+  };
+  Slot slots_[2];
+  int next_stage_ = 0, next_commit_ = 0, check_slot_ = 0;
+  bool check_pending_ = false;
+  cudaStream_t copy_ = nullptr;
+  unsigned long long* err_host_ = nullptr;
   unsigned long long* err_ = nullptr;
   double* loss_ = nullptr;
   void* flush_ = nullptr;
@@ -78,7 +99,6 @@ class EmbContext {
   int* bag_ = nullptr;
   int* skey_ = nullptr;
   int* sbag_ = nullptr;
-  long long* stage_idx_ = nullptr;
   int* unit_table_ = nullptr;
   int2* completers_ = nullptr;
   int4* completers_long_ = nullptr;

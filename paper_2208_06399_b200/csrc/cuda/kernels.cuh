@@ -164,16 +164,22 @@ __device__ __forceinline__ void cp_async_wait() {
 #define ASB_GATHER_U 4
 #endif
 constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
-constexpr int kStageX = 256;  // staged row ids per warp per buffer (R * SR)
-constexpr int kStageS = 288;  // staged keys per warp per buffer (R * (SR + 1))
+
+// Staged ints per warp and buffer for lane layout `kind`: row ids R*SR, keys R*(SR+1).
+__host__ __device__ constexpr int stage_x_ints(int kind) {
+  return kind <= 1 ? 256 : (kind <= 5 ? (32 >> kind) * 32 : 32);
+}
+__host__ __device__ constexpr int stage_s_ints(int kind) {
+  return kind == 0 ? 288 : (kind == 1 ? 272 : (kind <= 5 ? (32 >> kind) * 33 : 33));
+}
 
 template <bool FWD, int GL, int NV>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
+  const int kStageX = p.stage_x, kStageS = p.stage_s;
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
   constexpr int Q = SR / GL;                       // elements staged per lane per super-round
   constexpr int U = NV >= ASB_GATHER_U ? 1 : ASB_GATHER_U / NV;  // gathers in flight per lane
-  static_assert(R * SR <= kStageX && R * (SR + 1) <= kStageS, "stage too small");
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
   const int c = lane % GL;
@@ -339,15 +345,16 @@ template <bool FWD>
 #define ASB_SEG_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegParams p) {
-  __shared__ int xs[kSegWarps][2 * kStageX];
-  __shared__ int ss[kSegWarps][2 * kStageS];
+  // per warp: [2][stage_x] row ids then [2][stage_s] keys (sized on the host
+  // for the widest lane layout present in the shard)
+  extern __shared__ int seg_smem[];
   const int warp = threadIdx.x >> 5;
   const int unit = blockIdx.x * kSegWarps + warp;
   if (unit >= p.n_units) return;
   const int t = __ldg(p.unit_table + unit);
   const DevTable tb = p.tabs[t];
-  int* x = xs[warp];
-  int* s = ss[warp];
+  int* x = seg_smem + warp * 2 * (p.stage_x + p.stage_s);
+  int* s = x + 2 * p.stage_x;
   switch (tb.kind) {
     case 0: seg_unit<FWD, 1, 1>(p, tb, t, unit, x, s); break;
     case 1: seg_unit<FWD, 2, 1>(p, tb, t, unit, x, s); break;

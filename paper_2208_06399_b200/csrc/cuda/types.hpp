@@ -42,6 +42,8 @@ struct SegParams {
   // carries: [n_chunks][2][carry_stride] (0 = head, 1 = tail)
   float* carry;
   int carry_stride;
+  // index staging per warp and buffer (ints), sized for the shard's widest layout
+  int stage_x, stage_s;
   // chunks completing a segment that began in an earlier chunk: {chunk, table}
   int2* completers;
   int* n_completers;

@@ -106,6 +106,27 @@ class EmbeddingShard:
         check(lib().as_load_streams(self._h, po, pi, ni, _stream(stream)))
         self._keep = st
 
+    def stage(self, streams) -> None:
+        """Asynchronously copy the next batch to the device (see as_stage_streams)."""
+        if isinstance(streams, Workload):
+            check(lib().as_stage_workload(self._h, streams.handle))
+            return
+        st = [(np.ascontiguousarray(o, dtype=np.int64), np.ascontiguousarray(i, dtype=np.int64)) for o, i in streams]
+        n = max(1, len(st))
+        po = (C.c_void_p * n)(*[o.ctypes.data for o, _ in st])
+        pi = (C.c_void_p * n)(*[i.ctypes.data for _, i in st])
+        ni = (C.c_int64 * n)(*[len(i) for _, i in st])
+        check(lib().as_stage_streams(self._h, po, pi, ni))
+        self._staged_keep = getattr(self, "_staged_keep", [])[-1:] + [st]
+
+    def commit(self, stream=None) -> None:
+        """Pack + validate the oldest staged batch on `stream`; it becomes current."""
+        check(lib().as_commit_staged(self._h, _stream(stream)))
+
+    def check(self) -> None:
+        """Report OffsetError / IndexError of the last committed batch (synchronises)."""
+        check(lib().as_check_batch(self._h))
+
     # -- compute -----------------------------------------------------------
     def forward(self, out=None, stream=None) -> None:
         check(lib().as_forward(self._h, _ptr(out), _stream(stream)))

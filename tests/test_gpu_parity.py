@@ -298,3 +298,35 @@ def test_cfg2_full_size_properties(P, cuda):
                 g = G[bags[order[bounds[k]:bounds[k + 1]]]].sum(0)
                 want = (g @ g) / 128
                 assert abs(got[q] - want) <= 1e-5 * want + 1e-30
+
+
+def test_async_staging_pipeline_matches_sync_load(P, oracle, cuda):
+    """as_stage_* / as_commit_staged double buffering gives the same results as
+    the synchronous load, across alternating batches, and reports a bad batch."""
+    pool = P.generate_pool(2, 5, P.GeneratorConfig(dim_choices=(16, 64), hash_size_max=2e4))
+    B, seed = 256, 1
+    wls = [P.generate_workload(s, pool, B) for s in (10, 11, 12)]
+    ot = to_oracle_tables(pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.stage(wls[0])
+        sh.stage(wls[1])
+        with pytest.raises(P.StateError):
+            sh.stage(wls[2])  # two slots only
+        for k in range(3):
+            sh.commit()
+            if k + 2 < 3:
+                sh.stage(wls[k + 2])
+            sh.forward()
+            got = sh.read_pooled()
+            st = streams_of(wls[k], pool)
+            assert np.array_equal(got.astype(np.float64), oracle.forward_f64(ot, B, st, wseed=seed))
+        with pytest.raises(P.StateError):
+            sh.commit()  # nothing staged
+        bad = [(wls[0].find(t.id).offsets, wls[0].find(t.id).indices.copy()) for t in pool]
+        bad[3][1][0] = pool[3].hash_size
+        sh.stage(bad)
+        sh.commit()
+        with pytest.raises(P.IndexError_, match=f"table {pool[3].id}: index {pool[3].hash_size} out of range"):
+            sh.check()
+        with pytest.raises(P.StateError):
+            sh.forward()
