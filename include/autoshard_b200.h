@@ -181,15 +181,18 @@ AS_API as_status as_load_streams(as_ctx* ctx, const int64_t* const* offsets,
 AS_API as_status as_load_workload(as_ctx* ctx, const as_workload* wl, void* stream);
 
 /* Asynchronous, double-buffered loading for training loops: stage batch i+1
- * (host->device copy on the context's copy stream; returns without waiting
- * when the host buffers are pinned — they must stay valid until the copy
- * completes, i.e. until the matching as_commit_staged has been issued and the
- * stream reached it) while batch i computes, then commit it. as_commit_staged
- * packs + validates on `stream` (async) and makes it the current batch;
- * its OffsetError / IndexError is reported by as_check_batch, or by the next
- * synchronising call (as_step with a loss, as_measure, readbacks). Two slots:
- * staging a third batch before a commit returns AS_STATE. as_load_streams is
- * stage + commit + check. */
+ * while batch i computes, then commit it. as_stage_* returns immediately; a
+ * background job on the library's host thread pool narrows the int64 CSR to
+ * the device format (int32 global rows, rebased int32 offsets) into a pinned
+ * slot buffer, validating it like load_workload (workload_io.hpp:216-241),
+ * and enqueues each finished piece's host->device copy on the context's copy
+ * stream. The caller's host arrays must stay valid and unmodified until the
+ * matching as_commit_staged returns. as_commit_staged joins the job, reports
+ * the batch's first OffsetError / IndexError (table, check, entry order),
+ * and makes the slot the current batch (the compute `stream` waits for its
+ * copy). Two slots: staging a third batch before a commit returns AS_STATE.
+ * as_check_batch is kept for callers that separate commit and error checks
+ * (validation completes at commit). as_load_streams = stage + commit. */
 AS_API as_status as_stage_streams(as_ctx* ctx, const int64_t* const* offsets,
                                   const int64_t* const* indices, const int64_t* n_indices);
 AS_API as_status as_stage_workload(as_ctx* ctx, const as_workload* wl);

@@ -16,7 +16,11 @@
 #include "sort.cuh"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <mutex>
+
+#include "../host/threadpool.hpp"
 #include <cstring>
 
 namespace asb {
@@ -208,15 +212,14 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   W_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_w_)));
   M_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_rows_)));
   out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
-  off32_ = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
   for (Slot& sl : slots_) {
-    sl.off64 = static_cast<long long*>(dalloc(sizeof(long long) * static_cast<size_t>(T_ * (B_ + 1))));
+    sl.d_off32 = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
+    cuda_check(cudaHostAlloc(&sl.h_off32, sizeof(int) * static_cast<size_t>(T_ * B_ + 1), cudaHostAllocDefault),
+               "pinned staging");
     cuda_check(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&sl.retired, cudaEventDisableTiming), "event");
   }
   cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
-  cuda_check(cudaMallocHost(&err_host_, sizeof(unsigned long long)), "pinned err word");
-  *err_host_ = ~0ull;
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
   counters_ = static_cast<int*>(dalloc(sizeof(int) * 4));
@@ -272,10 +275,12 @@ EmbContext::~EmbContext() {
   if (side_) cudaStreamDestroy(side_);
   if (copy_) cudaStreamDestroy(copy_);
   for (Slot& sl : slots_) {
+    if (sl.job.joinable()) sl.job.join();
     if (sl.copied) cudaEventDestroy(sl.copied);
-    if (sl.consumed) cudaEventDestroy(sl.consumed);
+    if (sl.retired) cudaEventDestroy(sl.retired);
+    if (sl.h_idx32) cudaFreeHost(sl.h_idx32);
+    if (sl.h_off32) cudaFreeHost(sl.h_off32);
   }
-  if (err_host_) cudaFreeHost(err_host_);
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (prev >= 0) cudaSetDevice(prev);
@@ -290,9 +295,8 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   };
   if (L > cap_L_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
-    for (void* p : {(void*)idx32_, (void*)bag_, (void*)skey_, (void*)sbag_, cub_tmp_}) drop(p);
+    for (void* p : {(void*)bag_, (void*)skey_, (void*)sbag_, cub_tmp_}) drop(p);
     const int64_t cap = std::max<int64_t>(L + L / 8, 1024);
-    idx32_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     bag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     skey_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     sbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
@@ -323,8 +327,21 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   }
 }
 
-// ---- batch loading: stage (async H2D into one of two slots) -> commit
-// (pack + validate into the working arrays on the compute stream) -> check.
+// ---- batch loading -----------------------------------------------------------
+// stage(): lay the batch out on the host, then a background job narrows the
+//   caller's int64 CSR to the device format (int32 GLOBAL rows, rebased int32
+//   offsets) into a pinned slot buffer on the staging thread pool, validating
+//   with load_workload's checks (workload_io.hpp:216-241), and enqueues each
+//   finished piece's H2D on the copy stream right away (narrowing and PCIe
+//   overlap; the copy is half the bytes of the int64 source).
+// commit(): joins the job (raising the batch's first OffsetError /
+//   IndexError, in the reference's table/check/entry order) and swaps the
+//   slot's device arrays in as the current batch; the compute stream waits on
+//   the slot's copy event. Two slots: batch i+1 stages while batch i computes.
+namespace {
+constexpr int64_t kNarrowChunk = 1 << 20;
+}
+
 void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx) {
   DeviceGuard g(device_);
   Slot& sl = slots_[next_stage_];
@@ -361,30 +378,94 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   for (int t = 0; t < T_; ++t)
     std::fill(sl.utab.begin() + sl.tabs[t].unit_off, sl.utab.begin() + sl.tabs[t].unit_off + sl.tabs[t].n_units, t);
   if (L > sl.cap) {
+    // the slot's previous batch may still be in use on the device
     cuda_check(cudaDeviceSynchronize(), "grow sync");
-    if (sl.idx64) {
-      auto it = std::find(allocs_.begin(), allocs_.end(), (void*)sl.idx64);
+    auto drop = [this](void* p) {
+      auto it = std::find(allocs_.begin(), allocs_.end(), p);
       if (it != allocs_.end()) allocs_.erase(it);
-      cudaFree(sl.idx64);
-    }
+      cudaFree(p);
+    };
+    if (sl.d_idx32) drop(sl.d_idx32);
+    if (sl.h_idx32) cudaFreeHost(sl.h_idx32);
     sl.cap = std::max<int64_t>(L + L / 8, 1024);
-    sl.idx64 = static_cast<long long*>(dalloc(sizeof(long long) * sl.cap));
+    sl.d_idx32 = static_cast<int*>(dalloc(sizeof(int) * sl.cap));
+    cuda_check(cudaHostAlloc(&sl.h_idx32, sizeof(int) * sl.cap, cudaHostAllocDefault), "pinned staging");
   }
-  // the previous commit from this slot must have finished reading it
-  cuda_check(cudaStreamWaitEvent(copy_, sl.consumed, 0), "slot reuse");
-  // H2D: raw int64 CSR (pinned sources run at full PCIe rate on the copy engine)
-  for (int t = 0; t < T_; ++t) {
-    cuda_check(cudaMemcpyAsync(sl.off64 + (int64_t)t * (B_ + 1), offsets[t], sizeof(int64_t) * (B_ + 1),
-                               cudaMemcpyHostToDevice, copy_),
-               "offsets H2D");
-    if (n_idx[t] > 0)
-      cuda_check(cudaMemcpyAsync(sl.idx64 + sl.tabs[t].idx_off, indices[t], sizeof(int64_t) * n_idx[t],
-                                 cudaMemcpyHostToDevice, copy_),
-                 "indices H2D");
-  }
-  cuda_check(cudaEventRecord(sl.copied, copy_), "copied");
+  // nobody may still read the slot: its last commit's kernels (device) and
+  // its last H2D (host buffer reuse)
+  cuda_check(cudaEventSynchronize(sl.retired), "slot reuse");
+  cuda_check(cudaEventSynchronize(sl.copied), "slot reuse");
+  sl.err_key = ~0ull;
+  sl.err_val = 0;
   sl.staged = true;
   next_stage_ ^= 1;
+  // background job: narrow + validate + H2D, per table piece, on the pool
+  std::vector<std::array<int64_t, 3>> tasks;  // {table, begin, end}; begin = -1: offsets
+  for (int t = 0; t < T_; ++t) {
+    tasks.push_back({t, -1, 0});
+    for (int64_t b = 0; b < n_idx[t]; b += kNarrowChunk) tasks.push_back({t, b, std::min(n_idx[t], b + kNarrowChunk)});
+  }
+  std::vector<const int64_t*> off(offsets, offsets + T_), idx(indices, indices + T_);
+  Slot* sp = &sl;
+  const int dev = device_;
+  sl.job = std::thread([this, sp, dev, tasks = std::move(tasks), off = std::move(off), idx = std::move(idx)] {
+    try {
+      cudaSetDevice(dev);
+      std::mutex emu;
+      auto report = [&](int t, int kind, int64_t entry, int64_t value) {
+        const unsigned long long key =
+            ((unsigned long long)t << 42) | ((unsigned long long)kind << 40) | (unsigned long long)entry;
+        std::lock_guard<std::mutex> lk(emu);
+        if (key < sp->err_key) {
+          sp->err_key = key;
+          sp->err_val = value;
+        }
+      };
+      staging_pool().parallel_for((int64_t)tasks.size(), [&](int64_t k) {
+        const int t = (int)tasks[k][0];
+        const DevTable& d = sp->tabs[t];
+        if (tasks[k][1] < 0) {
+          const int64_t* o = off[t];
+          int* dst = sp->h_off32 + (int64_t)t * B_;
+          if (o[0] != 0) report(t, 0, 0, o[0]);
+          for (int64_t q = 0; q < B_; ++q) {
+            if (q > 0 && o[q] < o[q - 1]) report(t, 1, q, o[q]);
+            dst[q] = (int)(d.idx_off + o[q]);
+          }
+          if (B_ > 0 && o[B_] < o[B_ - 1]) report(t, 1, B_, o[B_]);
+          if (o[B_] != d.n_lookups) report(t, 2, B_, o[B_]);
+          if (t == T_ - 1) sp->h_off32[(int64_t)T_ * B_] = (int)(d.idx_off + d.n_lookups);
+          cuda_check(cudaMemcpyAsync(sp->d_off32 + (int64_t)t * B_, dst, sizeof(int) * (t == T_ - 1 ? B_ + 1 : B_),
+                                     cudaMemcpyHostToDevice, copy_),
+                     "offsets H2D");
+        } else {
+          const int64_t b = tasks[k][1], e = tasks[k][2];
+          const int64_t* src = idx[t];
+          int* dst = sp->h_idx32 + d.idx_off;
+          const int64_t hash = d.hash;
+          const int row0 = (int)d.row_off;
+          bool bad = false;
+          for (int64_t j = b; j < e; ++j) {
+            const int64_t v = src[j];
+            bad |= (v < 0) | (v >= hash);
+            dst[j] = row0 + (int)v;
+          }
+          if (bad)
+            for (int64_t j = b; j < e; ++j)
+              if (src[j] < 0 || src[j] >= hash) {
+                report(t, 3, j, src[j]);
+                break;
+              }
+          cuda_check(cudaMemcpyAsync(sp->d_idx32 + d.idx_off + b, dst + b, sizeof(int) * (e - b),
+                                     cudaMemcpyHostToDevice, copy_),
+                     "indices H2D");
+        }
+      });
+      cuda_check(cudaEventRecord(sp->copied, copy_), "copied");
+    } catch (...) {
+      sp->job_error = std::current_exception();
+    }
+  });
 }
 
 void EmbContext::commit(cudaStream_t s) {
@@ -392,13 +473,38 @@ void EmbContext::commit(cudaStream_t s) {
   Slot& sl = slots_[next_commit_];
   if (!sl.staged) fail(AS_STATE, "as_commit_staged: no staged batch");
   loaded_ = false;
+  sl.staged = false;
+  next_commit_ ^= 1;
+  if (sl.job.joinable()) sl.job.join();
+  if (sl.job_error) {
+    auto e = sl.job_error;
+    sl.job_error = nullptr;
+    std::rethrow_exception(e);
+  }
+  if (sl.err_key != ~0ull) {
+    const int t = static_cast<int>(sl.err_key >> 42);
+    const int kind = static_cast<int>((sl.err_key >> 40) & 3);
+    const int64_t q = static_cast<int64_t>(sl.err_key & ((1ull << 40) - 1));
+    const std::string where = "table " + std::to_string(specs_[t].id);
+    switch (kind) {
+      case 0: fail(AS_OFFSET, where + ": offsets must start at 0, got " + std::to_string(sl.err_val));
+      case 1: fail(AS_OFFSET, where + ": offsets must be nondecreasing at entry " + std::to_string(q));
+      case 2:
+        fail(AS_OFFSET, where + ": final offset " + std::to_string(sl.err_val) + " != index count " +
+                            std::to_string(sl.tabs[t].n_lookups));
+      default:
+        fail(AS_INDEX, where + ": index " + std::to_string(sl.err_val) + " out of range [0, " +
+                           std::to_string(specs_[t].hash_size) + ")");
+    }
+  }
   if (sort_pending_) {  // a forward's side-stream sort still reads the previous batch
     cuda_check(cudaStreamWaitEvent(s, ev_join_, 0), "join sort");
     sort_pending_ = false;
   }
-  if (sl.L > cap_L_ || sl.nch > cap_chunks_ || sl.nun > cap_units_)
-    cuda_check(cudaStreamSynchronize(s), "grow sync");
+  if (sl.L > cap_L_ || sl.nch > cap_chunks_ || sl.nun > cap_units_) cuda_check(cudaStreamSynchronize(s), "grow sync");
   ensure_capacity(sl.L, sl.nch, sl.nun);
+  // retire the batch being replaced, then swap the slot in
+  cuda_check(cudaEventRecord(cur_slot_ >= 0 ? slots_[cur_slot_].retired : sl.retired, s), "retire");
   cuda_check(cudaStreamWaitEvent(s, sl.copied, 0), "wait copy");
   htabs_ = sl.tabs;
   if (T_ > 0)
@@ -407,62 +513,17 @@ void EmbContext::commit(cudaStream_t s) {
   if (sl.nun > 0)
     cuda_check(cudaMemcpyAsync(unit_table_, sl.utab.data(), sizeof(int) * sl.nun, cudaMemcpyHostToDevice, s),
                "unit table H2D");
-  cuda_check(cudaMemsetAsync(err_, 0xff, sizeof(unsigned long long), s), "err reset");
-  if (T_ > 0) {
-    const long long n = (long long)T_ * (B_ + 1);
-    pack_offsets_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148LL * 32), 256, 0, s>>>(
-        sl.off64, T_, (int)B_, dtabs_, off32_, err_);
-    cuda_check(cudaGetLastError(), "pack_offsets_kernel");
-  }
-  if (sl.nun > 0) {
-    pack_indices_kernel<<<grid_for(sl.nun, kWarpsPerBlock), kBlock, 0, s>>>(sl.idx64, dtabs_, unit_table_,
-                                                                           (int)sl.nun, idx32_, err_);
-    cuda_check(cudaGetLastError(), "pack_indices_kernel");
-  }
-  cuda_check(cudaMemcpyAsync(err_host_, err_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "err D2H");
-  cuda_check(cudaEventRecord(sl.consumed, s), "consumed");
+  idx32_ = sl.d_idx32;
+  off32_ = sl.d_off32;
+  cur_slot_ = (int)(&sl - slots_);
   L_ = sl.L;
   n_chunks_ = sl.nch;
   n_units_ = sl.nun;
   loaded_ = true;
-  check_pending_ = true;
-  check_slot_ = next_commit_;
-  sl.staged = false;
-  next_commit_ ^= 1;
 }
 
-// Reports the validation result of the last commit (synchronises on it).
-void EmbContext::check() {
-  if (!check_pending_) return;
-  DeviceGuard g(device_);
-  const Slot& sl = slots_[check_slot_];
-  cuda_check(cudaEventSynchronize(sl.consumed), "load sync");
-  check_pending_ = false;
-  const unsigned long long err = *err_host_;
-  if (err == ~0ull) return;
-  loaded_ = false;
-  const int t = static_cast<int>(err >> 42);
-  const int kind = static_cast<int>((err >> 40) & 3);
-  const int64_t q = static_cast<int64_t>(err & ((1ull << 40) - 1));
-  const std::string where = "table " + std::to_string(specs_[t].id);
-  // the offending value is read back from the slot's staging copy
-  auto staged = [&](const long long* p) {
-    long long v = 0;
-    cuda_check(cudaMemcpy(&v, p, sizeof v, cudaMemcpyDeviceToHost), "err value D2H");
-    return v;
-  };
-  switch (kind) {
-    case 0:
-      fail(AS_OFFSET, where + ": offsets must start at 0, got " + std::to_string(staged(sl.off64 + (int64_t)t * (B_ + 1))));
-    case 1: fail(AS_OFFSET, where + ": offsets must be nondecreasing at entry " + std::to_string(q));
-    case 2:
-      fail(AS_OFFSET, where + ": final offset " + std::to_string(staged(sl.off64 + (int64_t)t * (B_ + 1) + B_)) +
-                          " != index count " + std::to_string(sl.tabs[t].n_lookups));
-    default:
-      fail(AS_INDEX, where + ": index " + std::to_string(staged(sl.idx64 + sl.tabs[t].idx_off + q)) +
-                         " out of range [0, " + std::to_string(specs_[t].hash_size) + ")");
-  }
-}
+// Validation now completes at commit; kept for the C-ABI contract.
+void EmbContext::check() {}
 
 void EmbContext::load(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx,
                       cudaStream_t s) {

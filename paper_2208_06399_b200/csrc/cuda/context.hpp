@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <string>
+#include <exception>
+#include <thread>
 #include <vector>
 
 #include "../host/host.hpp"
@@ -72,22 +74,27 @@ class EmbContext {
   float* W_ = nullptr;
   float* M_ = nullptr;
   float* out_ = nullptr;
-  int* off32_ = nullptr;
+  int* off32_ = nullptr;  // current batch (points into a slot)
   struct Slot {
-    long long* off64 = nullptr;  // [T*(B+1)] staged int64 offsets
-    long long* idx64 = nullptr;  // [cap] staged int64 indices
+    int* d_idx32 = nullptr;  // [cap] device: GLOBAL rows
+    int* d_off32 = nullptr;  // [T*B + 1] device: rebased offsets
+    int* h_idx32 = nullptr;  // pinned host staging of the same
+    int* h_off32 = nullptr;
     int64_t cap = 0;
     std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
     std::vector<int> utab;
     int64_t L = 0, nch = 0, nun = 0;
-    cudaEvent_t copied = nullptr, consumed = nullptr;
+    cudaEvent_t copied = nullptr;   // all H2D of the batch landed
+    cudaEvent_t retired = nullptr;  // the device no longer reads the batch
+    std::thread job;                // narrow + validate + H2D
+    std::exception_ptr job_error;
+    unsigned long long err_key = ~0ull;  // first validation error (table, kind, entry)
+    int64_t err_val = 0;
     bool staged = false;
   };
   Slot slots_[2];
-  int next_stage_ = 0, next_commit_ = 0, check_slot_ = 0;
-  bool check_pending_ = false;
+  int next_stage_ = 0, next_commit_ = 0, cur_slot_ = -1;
   cudaStream_t copy_ = nullptr;
-  unsigned long long* err_host_ = nullptr;
   unsigned long long* err_ = nullptr;
   double* loss_ = nullptr;
   void* flush_ = nullptr;

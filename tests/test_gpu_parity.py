@@ -325,8 +325,7 @@ def test_async_staging_pipeline_matches_sync_load(P, oracle, cuda):
         bad = [(wls[0].find(t.id).offsets, wls[0].find(t.id).indices.copy()) for t in pool]
         bad[3][1][0] = pool[3].hash_size
         sh.stage(bad)
-        sh.commit()
         with pytest.raises(P.IndexError_, match=f"table {pool[3].id}: index {pool[3].hash_size} out of range"):
-            sh.check()
+            sh.commit()
         with pytest.raises(P.StateError):
             sh.forward()
