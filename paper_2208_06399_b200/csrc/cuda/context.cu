@@ -339,13 +339,29 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
 //   slot's device arrays in as the current batch; the compute stream waits on
 //   the slot's copy event. Two slots: batch i+1 stages while batch i computes.
 namespace {
-constexpr int64_t kNarrowChunk = 1 << 20;
+constexpr int64_t kNarrowChunk = 1 << 19;
+
+// dst[j] = row0 + src[j]; returns true if any src[j] is outside [0, hash).
+// Multiversioned so the loop vectorises with AVX-512 / AVX2 where the host has it.
+__attribute__((target_clones("avx512f", "avx2", "default"))) bool narrow_rows(const int64_t* __restrict__ src,
+                                                                                int* __restrict__ dst, int64_t n,
+                                                                                int64_t hash, int row0) {
+  int64_t bad = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t v = src[j];
+    bad |= (int64_t)((uint64_t)v >= (uint64_t)hash);
+    dst[j] = row0 + (int)v;
+  }
+  return bad != 0;
+}
 }
 
 void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx) {
   DeviceGuard g(device_);
   Slot& sl = slots_[next_stage_];
-  if (sl.staged) fail(AS_STATE, "as_stage_streams: both staging slots hold uncommitted batches");
+  if (sl.staged || next_stage_ == cur_slot_)
+    fail(AS_STATE, "as_stage_streams: no free staging slot (one batch may be staged ahead of the current one; "
+                   "commit it first)");
   // Chunk length: ~128 KB of gathered rows per group, shrunk for small
   // batches so that there is at least about one wave of warps.
   double gbytes = 0.0;
@@ -443,13 +459,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
           const int64_t* src = idx[t];
           int* dst = sp->h_idx32 + d.idx_off;
           const int64_t hash = d.hash;
-          const int row0 = (int)d.row_off;
-          bool bad = false;
-          for (int64_t j = b; j < e; ++j) {
-            const int64_t v = src[j];
-            bad |= (v < 0) | (v >= hash);
-            dst[j] = row0 + (int)v;
-          }
+          const bool bad = narrow_rows(src + b, dst + b, e - b, hash, (int)d.row_off);
           if (bad)
             for (int64_t j = b; j < e; ++j)
               if (src[j] < 0 || src[j] >= hash) {

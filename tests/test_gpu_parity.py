@@ -314,14 +314,17 @@ def test_async_staging_pipeline_matches_sync_load(P, oracle, cuda):
             sh.stage(wls[2])  # two slots only
         for k in range(3):
             sh.commit()
-            if k + 2 < 3:
-                sh.stage(wls[k + 2])
+            with pytest.raises(P.StateError):
+                if k == 0:
+                    sh.stage(wls[2])  # slot of the current batch is busy, the other is staged
+                else:
+                    sh.commit()  # nothing staged
+            if k == 1:
+                sh.stage(wls[2])
             sh.forward()
             got = sh.read_pooled()
             st = streams_of(wls[k], pool)
             assert np.array_equal(got.astype(np.float64), oracle.forward_f64(ot, B, st, wseed=seed))
-        with pytest.raises(P.StateError):
-            sh.commit()  # nothing staged
         bad = [(wls[0].find(t.id).offsets, wls[0].find(t.id).indices.copy()) for t in pool]
         bad[3][1][0] = pool[3].hash_size
         sh.stage(bad)
