@@ -20,6 +20,8 @@
 #include <cmath>
 #include <mutex>
 
+#include <immintrin.h>
+
 #include "../host/threadpool.hpp"
 #include <cstring>
 
@@ -245,6 +247,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
 
   // K6: weights from the counter hash, momentum zero.
   const unsigned long long s0 = splitmix64(seed_);
@@ -283,6 +286,7 @@ EmbContext::~EmbContext() {
   }
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_done_) cudaEventDestroy(ev_done_);
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -342,10 +346,36 @@ namespace {
 constexpr int64_t kNarrowChunk = 1 << 19;
 
 // dst[j] = row0 + src[j]; returns true if any src[j] is outside [0, hash).
-// Multiversioned so the loop vectorises with AVX-512 / AVX2 where the host has it.
-__attribute__((target_clones("avx512f", "avx2", "default"))) bool narrow_rows(const int64_t* __restrict__ src,
-                                                                                int* __restrict__ dst, int64_t n,
-                                                                                int64_t hash, int row0) {
+// The AVX-512 path uses streaming (non-temporal) stores into the pinned
+// staging buffer: host memory bandwidth bounds this loop, and streaming
+// stores skip the read-for-ownership of the destination lines.
+__attribute__((target("avx512f"))) bool narrow_rows_avx512(const int64_t* __restrict__ src, int* __restrict__ dst,
+                                                           int64_t n, int64_t hash, int row0) {
+  int64_t j = 0;
+  int64_t bad = 0;
+  while (j < n && (reinterpret_cast<uintptr_t>(dst + j) & 31)) {
+    bad |= (int64_t)((uint64_t)src[j] >= (uint64_t)hash);
+    dst[j] = row0 + (int)src[j];
+    ++j;
+  }
+  const __m512i vh = _mm512_set1_epi64(hash);
+  const __m256i vr = _mm256_set1_epi32(row0);
+  __mmask8 m = 0;
+  for (; j + 8 <= n; j += 8) {
+    const __m512i v = _mm512_loadu_si512(src + j);
+    m |= _mm512_cmpge_epu64_mask(v, vh);
+    const __m256i w = _mm256_add_epi32(_mm512_cvtepi64_epi32(v), vr);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + j), w);
+  }
+  for (; j < n; ++j) {
+    bad |= (int64_t)((uint64_t)src[j] >= (uint64_t)hash);
+    dst[j] = row0 + (int)src[j];
+  }
+  _mm_sfence();
+  return bad != 0 || m != 0;
+}
+
+bool narrow_rows_scalar(const int64_t* __restrict__ src, int* __restrict__ dst, int64_t n, int64_t hash, int row0) {
   int64_t bad = 0;
   for (int64_t j = 0; j < n; ++j) {
     const int64_t v = src[j];
@@ -353,6 +383,11 @@ __attribute__((target_clones("avx512f", "avx2", "default"))) bool narrow_rows(co
     dst[j] = row0 + (int)v;
   }
   return bad != 0;
+}
+
+bool narrow_rows(const int64_t* src, int* dst, int64_t n, int64_t hash, int row0) {
+  static const bool avx512 = __builtin_cpu_supports("avx512f");
+  return avx512 ? narrow_rows_avx512(src, dst, n, hash, row0) : narrow_rows_scalar(src, dst, n, hash, row0);
 }
 }
 
@@ -662,7 +697,9 @@ void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
   backward(out_, lr, eps, s);
   if (loss_host) {
     cuda_check(cudaMemcpyAsync(loss_host, loss_, sizeof(double), cudaMemcpyDeviceToHost, s), "loss D2H");
-    cuda_check(cudaStreamSynchronize(s), "step sync");
+    // sleep (not spin) until the step is done: the staging pool needs the cores
+    cuda_check(cudaEventRecord(ev_done_, s), "done");
+    cuda_check(cudaEventSynchronize(ev_done_), "step sync");
     check();  // report a bad batch with the step's result
   }
 }

@@ -119,7 +119,7 @@ class EmbContext {
   size_t cub_bytes_ = 0;
 
   cudaStream_t side_ = nullptr;  // K2 sort overlapped with the forward
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_done_ = nullptr;
   bool sort_pending_ = false;
   int64_t L_ = 0;
   int64_t n_chunks_ = 0;
