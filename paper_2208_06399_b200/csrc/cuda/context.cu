@@ -393,10 +393,13 @@ bool narrow_rows(const int64_t* src, int* dst, int64_t n, int64_t hash, int row0
 
 void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx) {
   DeviceGuard g(device_);
-  Slot& sl = slots_[next_stage_];
-  if (sl.staged || next_stage_ == cur_slot_)
+  int pick = -1;
+  for (int k = 0; k < 2 && pick < 0; ++k)
+    if (!slots_[k].staged && k != cur_slot_) pick = k;
+  if (pick < 0)
     fail(AS_STATE, "as_stage_streams: no free staging slot (one batch may be staged ahead of the current one; "
                    "commit it first)");
+  Slot& sl = slots_[pick];
   // Chunk length: ~128 KB of gathered rows per group, shrunk for small
   // batches so that there is at least about one wave of warps.
   double gbytes = 0.0;
@@ -449,7 +452,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   sl.err_key = ~0ull;
   sl.err_val = 0;
   sl.staged = true;
-  next_stage_ ^= 1;
+  sl.seq = ++stage_seq_;
   // background job: narrow + validate + H2D, per table piece, on the pool
   std::vector<std::array<int64_t, 3>> tasks;  // {table, begin, end}; begin = -1: offsets
   for (int t = 0; t < T_; ++t) {
@@ -515,11 +518,13 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
 
 void EmbContext::commit(cudaStream_t s) {
   DeviceGuard g(device_);
-  Slot& sl = slots_[next_commit_];
-  if (!sl.staged) fail(AS_STATE, "as_commit_staged: no staged batch");
+  int pick = -1;
+  for (int k = 0; k < 2; ++k)
+    if (slots_[k].staged && (pick < 0 || slots_[k].seq < slots_[pick].seq)) pick = k;  // oldest first
+  if (pick < 0) fail(AS_STATE, "as_commit_staged: no staged batch");
+  Slot& sl = slots_[pick];
   loaded_ = false;
   sl.staged = false;
-  next_commit_ ^= 1;
   if (sl.job.joinable()) sl.job.join();
   if (sl.job_error) {
     auto e = sl.job_error;

@@ -91,9 +91,11 @@ class EmbContext {
     unsigned long long err_key = ~0ull;  // first validation error (table, kind, entry)
     int64_t err_val = 0;
     bool staged = false;
+    uint64_t seq = 0;  // staging order (commit takes the oldest)
   };
   Slot slots_[2];
-  int next_stage_ = 0, next_commit_ = 0, cur_slot_ = -1;
+  int cur_slot_ = -1;
+  uint64_t stage_seq_ = 0;
   cudaStream_t copy_ = nullptr;
   unsigned long long* err_ = nullptr;
   double* loss_ = nullptr;
