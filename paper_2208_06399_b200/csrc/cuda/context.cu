@@ -12,6 +12,7 @@
 //   pooled fp32 [B, sum dim_t], table columns in context order
 #include "context.hpp"
 #include "kernels.cuh"
+#include "seg_tma.cuh"
 
 #include "sort.cuh"
 
@@ -23,6 +24,7 @@
 #include <immintrin.h>
 
 #include "../host/threadpool.hpp"
+#include <cstdlib>
 #include <cstring>
 
 namespace asb {
@@ -244,6 +246,13 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
   }
+  if (const char* e = std::getenv("ASB_TMA")) use_tma_ = std::atoi(e) != 0;
+  cuda_check(cudaFuncSetAttribute(seg_reduce_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kTmaSmemBytes),
+             "tma smem");
+  cuda_check(cudaFuncSetAttribute(seg_reduce_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kTmaSmemBytes),
+             "tma smem");
   cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
@@ -407,6 +416,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   const double target = std::max(2048.0, std::min(131072.0, gbytes / (148.0 * 24.0)));
   sl.tabs = htabs_;
   int64_t L = 0, nch = 0, nun = 0;
+  std::vector<int64_t> units_of(static_cast<size_t>(T_));
   for (int t = 0; t < T_; ++t) {
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
     DevTable& d = sl.tabs[t];
@@ -414,15 +424,25 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
     const int R = 32 >> std::min(d.kind, 5);
     const int64_t chunks = (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
     const int64_t units = (chunks + R - 1) / R;
+    units_of[t] = units;
     d.idx_off = L;
     d.n_lookups = n_idx[t];
     d.chunk_off = static_cast<int>(nch);
-    d.unit_off = static_cast<int>(nun);
     d.n_units = static_cast<int>(units);
     L += n_idx[t];
     nch += units * R;
-    nun += units;
   }
+  // warp units: tables on the TMA path (rows >= 100 floats) first, one launch each
+  for (int pass = 0; pass < 2; ++pass)
+    for (int t = 0; t < T_; ++t) {
+      const bool tma = use_tma_ && sl.tabs[t].kind >= 5;
+      if (tma != (pass == 0)) continue;
+      sl.tabs[t].unit_off = static_cast<int>(nun);
+      nun += units_of[t];
+    }
+  sl.n_tma_units = 0;
+  for (int t = 0; t < T_; ++t)
+    if (use_tma_ && sl.tabs[t].kind >= 5) sl.n_tma_units += units_of[t];
   if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
   if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
   sl.L = L;
@@ -569,6 +589,7 @@ void EmbContext::commit(cudaStream_t s) {
   L_ = sl.L;
   n_chunks_ = sl.nch;
   n_units_ = sl.nun;
+  n_tma_units_ = sl.n_tma_units;
   loaded_ = true;
 }
 
@@ -605,6 +626,25 @@ SegParams EmbContext::seg_params(bool fwd) const {
   return p;
 }
 
+// K1 / K3 launches: the TMA-gather kernel for the units of wide-row tables,
+// the register-gather kernel for the rest.
+template <bool FWD>
+void EmbContext::launch_seg(SegParams p, cudaStream_t s) {
+  if (n_tma_units_ > 0) {
+    p.unit_begin = 0;
+    seg_reduce_tma_kernel<FWD><<<grid_for(n_tma_units_, kTmaWarps), kTmaWarps * 32, kTmaSmemBytes, s>>>(
+        p, (int)n_tma_units_);
+    cuda_check(cudaGetLastError(), "seg_reduce_tma_kernel");
+    ++launches_;
+  }
+  if (n_units_ > n_tma_units_) {
+    p.unit_begin = (int)n_tma_units_;
+    seg_reduce_kernel<FWD><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
+    cuda_check(cudaGetLastError(), "seg_reduce_kernel");
+    ++launches_;
+  }
+}
+
 void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   require_loaded("as_forward");
   DeviceGuard g(device_);
@@ -631,12 +671,10 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.out = target;
   p.out_stride = sum_dim_;
   p.loss = loss_dev;
-  const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
   cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 1, s);
-    seg_reduce_kernel<true><<<grid, kBlock, seg_smem_bytes_, s>>>(p);
-    cuda_check(cudaGetLastError(), "seg_reduce_kernel<fwd>");
+    launch_seg<true>(p, s);
   }
   {
     Phase ph(this, 2, s);
@@ -678,12 +716,10 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   p.M = M_;
   p.lr = lr;
   p.eps = eps;
-  const unsigned grid = grid_for(n_units_, kWarpsPerBlock);
   cuda_check(cudaMemsetAsync(counters_ + 2, 0, sizeof(int) * 2, s), "counter reset");
   {
     Phase ph(this, 4, s);
-    seg_reduce_kernel<false><<<grid, kBlock, seg_smem_bytes_, s>>>(p);
-    cuda_check(cudaGetLastError(), "seg_reduce_kernel<bwd>");
+    launch_seg<false>(p, s);
   }
   {
     Phase ph(this, 5, s);
@@ -691,7 +727,7 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
     seg_fixup_long_kernel<false><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
   }
-  launches_ += 3;
+  launches_ += 2;
 }
 
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {

@@ -57,6 +57,8 @@ class EmbContext {
   void* dalloc(size_t bytes);
   SegParams seg_params(bool fwd) const;
   void launch_sort(cudaStream_t s);
+  template <bool FWD>
+  void launch_seg(SegParams p, cudaStream_t s);
 
   int device_;
   int T_;
@@ -83,7 +85,7 @@ class EmbContext {
     int64_t cap = 0;
     std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
     std::vector<int> utab;
-    int64_t L = 0, nch = 0, nun = 0;
+    int64_t L = 0, nch = 0, nun = 0, n_tma_units = 0;
     cudaEvent_t copied = nullptr;   // all H2D of the batch landed
     cudaEvent_t retired = nullptr;  // the device no longer reads the batch
     std::thread job;                // narrow + validate + H2D
@@ -116,6 +118,8 @@ class EmbContext {
   unsigned fixup_short_grid_ = 2368;
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
+  int64_t n_tma_units_ = 0;
+  bool use_tma_ = true;  // ASB_TMA=0 forces the register-gather kernel (A/B)
   float* carry_ = nullptr;
   void* cub_tmp_ = nullptr;
   size_t cub_bytes_ = 0;

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegP
   // for the widest lane layout present in the shard)
   extern __shared__ int seg_smem[];
   const int warp = threadIdx.x >> 5;
-  const int unit = blockIdx.x * kSegWarps + warp;
+  const int unit = p.unit_begin + blockIdx.x * kSegWarps + warp;
   if (unit >= p.n_units) return;
   const int t = __ldg(p.unit_table + unit);
   const DevTable tb = p.tabs[t];

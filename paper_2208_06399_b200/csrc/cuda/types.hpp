@@ -26,6 +26,7 @@ struct SegParams {
   const DevTable* tabs;
   const int* unit_table;  // warp unit -> table position
   int n_units;
+  int unit_begin;  // first unit handled by this launch
   const int* seg;  // segment key per element
   const int* src;  // gathered row per element
   // forward
