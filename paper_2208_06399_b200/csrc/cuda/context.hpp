@@ -119,7 +119,7 @@ class EmbContext {
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
   int64_t n_tma_units_ = 0;
-  bool use_tma_ = true;  // ASB_TMA=0 forces the register-gather kernel (A/B)
+  bool use_tma_ = false;  // ASB_TMA=1: TMA bulk-copy gathers for wide rows (measured 3x slower)
   float* carry_ = nullptr;
   void* cub_tmp_ = nullptr;
   size_t cub_bytes_ = 0;
