@@ -173,7 +173,9 @@ __host__ __device__ constexpr int stage_s_ints(int kind) {
   return kind == 0 ? 288 : (kind == 1 ? 272 : (kind <= 5 ? (32 >> kind) * 33 : 33));
 }
 
-template <bool FWD, int GL, int NV>
+// EXACT: dim == 4*GL*NV, so every lane owns a full column slice and the gathers
+// need no column predicate.
+template <bool FWD, int GL, int NV, bool EXACT>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
   const int kStageX = p.stage_x, kStageS = p.stage_s;
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
@@ -194,16 +196,17 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const bool live = j_lo < j_hi;
   const int prev_seg = (live && j_lo > t_lo) ? __ldg(p.seg + j_lo - 1) : -1;
 
-  const float* gbase;
+  // gathered row = gbase + row_id * gstride (bytes): one IMAD.WIDE.U32 per gather
+  const char* gbase;
   unsigned gstride;
   if constexpr (FWD) {
-    gbase = p.W_ro + tb.w_base;
-    gstride = (unsigned)tb.dim;
+    gbase = reinterpret_cast<const char*>(p.W_ro + tb.w_base);
+    gstride = (unsigned)tb.dim * 4u;
   } else {
-    gbase = p.grad + tb.col;
-    gstride = (unsigned)p.grad_stride;
+    gbase = reinterpret_cast<const char*>(p.grad + tb.col);
+    gstride = (unsigned)p.grad_stride * 4u;
   }
-  gbase += c * 4;
+  gbase += c * 16;
 
   // stage the row ids [base, base+SR) and keys [base, base+SR] of one super-round
   auto stage = [&](long long base, int buf) {
@@ -275,13 +278,26 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
         }
       }
       float4 v[U][NV];
+      if (m0 + U <= nval) {  // full batch: no element predicate
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool ok = m0 + u < nval;
-        const float* row = gbase + (size_t)((unsigned)gx[m0 + u]) * gstride;
+        for (int u = 0; u < U; ++u) {
+          const char* row = gbase + (size_t)(unsigned)gx[m0 + u] * gstride;
 #pragma unroll
-        for (int w = 0; w < NV; ++w)
-          v[u][w] = (ok && c + w * GL < nvec) ? ldg4(row + w * GL * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int w = 0; w < NV; ++w)
+            v[u][w] = (EXACT || c + w * GL < nvec) ? ldg4(reinterpret_cast<const float*>(row + w * GL * 16))
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = m0 + u < nval;
+          const char* row = gbase + (size_t)(unsigned)gx[m0 + u] * gstride;
+#pragma unroll
+          for (int w = 0; w < NV; ++w)
+            v[u][w] = (ok && (EXACT || c + w * GL < nvec))
+                          ? ldg4(reinterpret_cast<const float*>(row + w * GL * 16))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       if (ebits == 0) {
 #pragma unroll
@@ -355,17 +371,32 @@ __global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegP
   const DevTable tb = p.tabs[t];
   int* x = seg_smem + warp * 2 * (p.stage_x + p.stage_s);
   int* s = x + 2 * p.stage_x;
+  // lane layouts; "exact" widths (dim = 4*GL*NV) drop the column predicate
+  const bool ex = tb.dim == 4 * (tb.kind <= 5 ? (1 << tb.kind) : 32) * (tb.kind <= 5 ? 1 : 1 << (tb.kind - 5));
+#define ASB_SEG_CASE(K, GLV, NVV)                                    \
+  case K:                                                            \
+    if (ex)                                                          \
+      seg_unit<FWD, GLV, NVV, true>(p, tb, t, unit, x, s);           \
+    else                                                             \
+      seg_unit<FWD, GLV, NVV, false>(p, tb, t, unit, x, s);          \
+    break;
   switch (tb.kind) {
-    case 0: seg_unit<FWD, 1, 1>(p, tb, t, unit, x, s); break;
-    case 1: seg_unit<FWD, 2, 1>(p, tb, t, unit, x, s); break;
-    case 2: seg_unit<FWD, 4, 1>(p, tb, t, unit, x, s); break;
-    case 3: seg_unit<FWD, 8, 1>(p, tb, t, unit, x, s); break;
-    case 4: seg_unit<FWD, 16, 1>(p, tb, t, unit, x, s); break;
-    case 5: seg_unit<FWD, 32, 1>(p, tb, t, unit, x, s); break;
-    case 6: seg_unit<FWD, 32, 2>(p, tb, t, unit, x, s); break;
-    case 7: seg_unit<FWD, 32, 4>(p, tb, t, unit, x, s); break;
-    default: seg_unit<FWD, 32, 8>(p, tb, t, unit, x, s); break;
+    ASB_SEG_CASE(0, 1, 1)
+    ASB_SEG_CASE(1, 2, 1)
+    ASB_SEG_CASE(2, 4, 1)
+    ASB_SEG_CASE(3, 8, 1)
+    ASB_SEG_CASE(4, 16, 1)
+    ASB_SEG_CASE(5, 32, 1)
+    ASB_SEG_CASE(6, 32, 2)
+    ASB_SEG_CASE(7, 32, 4)
+    default:
+      if (ex)
+        seg_unit<FWD, 32, 8, true>(p, tb, t, unit, x, s);
+      else
+        seg_unit<FWD, 32, 8, false>(p, tb, t, unit, x, s);
+      break;
   }
+#undef ASB_SEG_CASE
 }
 
 // ---- fixups -----------------------------------------------------------------
