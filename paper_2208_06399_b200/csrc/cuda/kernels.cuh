@@ -113,6 +113,41 @@ __device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& 
   if (c == 0) p.M[seg] = m;
 }
 
+// Predicated variant for lane groups that run converged (GL < 32): every lane
+// of the warp executes it (the group reduction needs them), `active` selects
+// the groups whose segment ends here.
+template <int GL, int NV>
+__device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTable& tb, int seg, const float4 (&g)[NV],
+                                                 int c, bool active) {
+  const int nvec = tb.dim >> 2;
+  float sq = 0.f;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    if (c + q * GL < nvec) sq += f4dot(g[q]);
+  sq = group_sum<GL>(sq, 0xffffffffu);
+  if (active) {
+    float4 w[NV];
+    float m_old;
+    load_row_state<GL, NV>(p, tb, seg, c, w, m_old);
+    const float m = m_old + sq / (float)tb.dim;
+    const float mult = p.lr / (sqrtf(m) + p.eps);
+    float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      const int cv = c + q * GL;
+      if (cv < nvec) {
+        float4 x = w[q];
+        x.x -= mult * g[q].x;
+        x.y -= mult * g[q].y;
+        x.z -= mult * g[q].z;
+        x.w -= mult * g[q].w;
+        *reinterpret_cast<float4*>(wr + cv * 4) = x;
+      }
+    }
+    if (c == 0) p.M[seg] = m;
+  }
+}
+
 template <bool FWD, int GL, int NV>
 __device__ __forceinline__ void finish_segment(const SegParams& p, const DevTable& tb, unsigned gmask, int seg,
                                                const float4 (&v)[NV], int c, float& loss_acc) {
@@ -266,17 +301,6 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll 1
     for (int m0 = 0; m0 < SR; m0 += U) {
       unsigned ebits = (endm >> m0) & low_bits<U>();
-      // backward: the first segment ending in this batch gets its row state
-      // fetched together with the gathers
-      float4 wpre[FWD ? 1 : NV];
-      float mpre = 0.f;
-      int spre = -7;
-      if constexpr (!FWD) {
-        if (ebits) {
-          spre = gs[m0 + __ffs(ebits) - 1];
-          if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
-        }
-      }
       float4 v[U][NV];
       if (m0 + U <= nval) {  // full batch: no element predicate
 #pragma unroll
@@ -299,42 +323,81 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      if (ebits == 0) {
+      if constexpr (GL < 32) {
+        // several chunks per warp: stay converged, handle each element's
+        // segment end with a warp-uniform test and predicated epilogues
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+        for (int u = 0; u < U; ++u) {
 #pragma unroll
           for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
-      } else {
-        int u0 = 0;
-        for (;;) {  // group-uniform
-          const int e = ebits ? __ffs(ebits) - 1 : U;
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (u >= u0 && u <= e)
-#pragma unroll
-              for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
-          if (e >= U) break;
-          const int s = gs[m0 + e];
-          if (s == prev_seg) {
-            // completes a segment that began in an earlier chunk -> fixup
-            store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
-            if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
-          } else if constexpr (FWD) {
-            store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
-          } else {
-            if (s == spre) {
-              adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wpre, mpre);
+          const bool endu = (ebits >> u) & 1u;
+          if (__any_sync(0xffffffffu, endu)) {
+            const int s = gs[m0 + u];
+            const bool split = s == prev_seg;
+            if (endu && split) {
+              store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
+              if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
+            }
+            if constexpr (FWD) {
+              if (endu && !split) store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
             } else {
-              float4 wr[NV];
-              float mr;
-              load_row_state<GL, NV>(p, tb, s, c, wr, mr);
-              adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wr, mr);
+              adagrad_row_pred<GL, NV>(p, tb, s, acc, c, endu && !split);
+            }
+            if (endu) {
+#pragma unroll
+              for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
+        }
+      } else {
+      // backward: the first segment ending in this batch gets its row state
+      // fetched together with the gathers
+      float4 wpre[FWD ? 1 : NV];
+      float mpre = 0.f;
+      int spre = -7;
+      if constexpr (!FWD) {
+        if (ebits) {
+          spre = gs[m0 + __ffs(ebits) - 1];
+          if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
+        }
+      }
+        if (ebits == 0) {
 #pragma unroll
-          for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
-          ebits &= ebits - 1;
-          u0 = e + 1;
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
+        } else {
+          int u0 = 0;
+          for (;;) {  // group-uniform
+            const int e = ebits ? __ffs(ebits) - 1 : U;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (u >= u0 && u <= e)
+#pragma unroll
+                for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
+            if (e >= U) break;
+            const int s = gs[m0 + e];
+            if (s == prev_seg) {
+              // completes a segment that began in an earlier chunk -> fixup
+              store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
+              if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
+            } else if constexpr (FWD) {
+              store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
+            } else {
+              if (s == spre) {
+                adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wpre, mpre);
+              } else {
+                float4 wr[NV];
+                float mr;
+                load_row_state<GL, NV>(p, tb, s, c, wr, mr);
+                adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wr, mr);
+              }
+            }
+#pragma unroll
+            for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+            ebits &= ebits - 1;
+            u0 = e + 1;
+          }
         }
       }
     }
