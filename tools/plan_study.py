@@ -1,0 +1,84 @@
+#!/usr/bin/env python
+"""Sharding-plan study on MEASURED B200 shard times (§5).
+
+For a BASELINE config, builds the comparison plans — size/dim/lookup greedy
+(planners.hpp:73-107), random (planners.hpp:111-136, several seeds) and, when
+present, an AutoShard-RL plan produced by the reference trainer
+(oracle/rl_plans.cpp -> plans/<cfg>_autoshard_rl.assignment) — and measures
+every shard of every plan with the GPU cost hook (`measure_plan`: W=5/B=10/R=2
+fwd+bwd+row-wise Adagrad steps, L2 flushed). Shards run one at a time on one
+GPU (the paper's per-device micro-benchmark). Reports max-shard ms (the C_k
+objective), degree of balance and speedups.
+
+  python tools/plan_study.py --workload cfg3 --out profiles/plan_study_cfg3.json
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2208_06399_b200 as P  # noqa: E402
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg3")
+    ap.add_argument("--shards", type=int, default=8)
+    ap.add_argument("--random-seeds", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--measure", type=int, default=10)
+    ap.add_argument("--trim", type=int, default=2)
+    args = ap.parse_args()
+
+    tables, B, desc = bench.build_workload(P, args.workload)
+    K = args.shards
+    wl = P.generate_workload(0, tables, B).pin()
+    total = sum(t.size_bytes() for t in tables)
+    task = P.ShardingTask(tables, K, [int(1.6 * total / K)] * K)  # SPEC.md:620 budget rule
+    plans = {}
+    for kind, name in [(P.HeuristicKind.kSizeGreedy, "size-greedy"), (P.HeuristicKind.kDimGreedy, "dim-greedy"),
+                       (P.HeuristicKind.kLookupGreedy, "lookup-greedy")]:
+        plans[name] = P.greedy_shard(task, kind)
+    for s in range(args.random_seeds):
+        plans[f"random-{s}"] = P.random_shard(task, s)
+    rl = os.path.join(ROOT, "plans", f"{args.workload}_autoshard_rl.assignment")
+    if os.path.exists(rl):
+        a = [int(x) for x in open(rl).read().split()]
+        if len(a) == len(tables):
+            plans["autoshard-rl"] = P.ShardingPlan(a)
+    bench_cfg = P.BenchConfig(warmup=args.warmup, measure=args.measure, trim=args.trim)
+    res = {}
+    for name, plan in plans.items():
+        t0 = time.time()
+        costs = P.measure_plan(plan, task, wl, bench_cfg)
+        res[name] = {"assignment": plan.assignment, "shard_ms": costs, "max_ms": max(costs),
+                     "balance": P.degree_of_balance(costs), "feasible": plan.feasible(task),
+                     "wall_s": round(time.time() - t0, 1)}
+        print(f"{name:14s} max {max(costs):7.3f} ms  balance {res[name]['balance']:.3f}  "
+              f"shards {' '.join(f'{c:.3f}' for c in costs)}", flush=True)
+    rnd = [res[k]["max_ms"] for k in res if k.startswith("random-")]
+    rnd_mean = sum(rnd) / len(rnd)
+    for k, v in res.items():
+        v["speedup_vs_random_mean"] = rnd_mean / v["max_ms"]
+        v["speedup_vs_lookup_greedy"] = res["lookup-greedy"]["max_ms"] / v["max_ms"]
+    out = {"workload": args.workload, "desc": desc, "shards": K, "batch": B,
+           "budget_rule": "1.6 x total / K (SPEC.md:620), bytes_per_param 2",
+           "protocol": f"W={args.warmup} B={args.measure} R={args.trim}, L2 flushed, one shard at a time on 1 GPU",
+           "random_max_ms_mean": rnd_mean, "plans": res}
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(out, f, indent=1)
+    print(json.dumps({k: {"max_ms": round(v["max_ms"], 3), "balance": round(v["balance"], 3),
+                          "speedup_vs_random": round(v["speedup_vs_random_mean"], 3),
+                          "speedup_vs_lookup_greedy": round(v["speedup_vs_lookup_greedy"], 3)}
+                      for k, v in res.items()}))
+
+
+if __name__ == "__main__":
+    main()
