@@ -260,6 +260,13 @@ AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info);
 AS_API as_status as_profile_enable(as_ctx* ctx, int32_t enable);
 AS_API as_status as_profile_read(as_ctx* ctx, double* ms_per_phase, int64_t* launches, int32_t reset);
 
+/* Cost-model features of the loaded batch, computed on the
+ * device from the backward's sorted keys instead of a host hash map:
+ * out[t*21 + :] = FeatureVector::raw of extract_features (tables.hpp:344-386):
+ * dim, hash_size, observed pooling, size_gb, 17 frequency-bin ratios over the
+ * table's distinct rows. Synchronises. */
+AS_API as_status as_table_features(as_ctx* ctx, double* out, void* stream);
+
 /* Readbacks for parity (synchronise). */
 /* rows: n row ids (table-local) of ctx table position t -> out [n, dim] fp32. */
 AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out);

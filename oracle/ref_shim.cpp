@@ -252,4 +252,16 @@ int ref_measure_plan(const RefTable* t, int n, int k, const int64_t* budgets,
   })
 }
 
+// extract_features raw vectors (tables.hpp:344-386), identity norm stats.
+int ref_extract_features(const RefTable* t, int n, void* handle, double* out) {
+  REF_TRY({
+    auto* w = static_cast<RefWorkload*>(handle);
+    autoshard::NormStats ns;
+    for (int i = 0; i < n; ++i) {
+      const auto f = autoshard::extract_features(to_desc(t[i]), w->wl, ns);
+      for (int k = 0; k < autoshard::kNumFeatures; ++k) out[i * autoshard::kNumFeatures + k] = f.raw[k];
+    }
+  })
+}
+
 }  // extern "C"

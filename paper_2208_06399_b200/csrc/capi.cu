@@ -475,6 +475,14 @@ AS_API as_status as_profile_read(as_ctx* ctx, double* ms, int64_t* launches, int
   });
 }
 
+AS_API as_status as_table_features(as_ctx* ctx, double* out, void* stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->impl->table_features(out, static_cast<cudaStream_t>(stream));
+  });
+}
+
 AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out) {
   return guard([&] {
     need(ctx, "ctx");

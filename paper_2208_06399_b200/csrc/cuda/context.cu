@@ -778,6 +778,50 @@ double EmbContext::measure(int warmup, int measure, int trim, bool flush, float 
   return sum / static_cast<double>(measure - 2 * trim);
 }
 
+// Raw cost-model features of the loaded batch, laid out like FeatureVector::raw
+// (tables.hpp:300-386): [dim, hash_size, observed pooling, size_gb, 17 bins].
+void EmbContext::table_features(double* out, cudaStream_t s) {
+  check();
+  require_loaded("as_table_features");
+  DeviceGuard g(device_);
+  std::vector<unsigned long long> hist(static_cast<size_t>(std::max(1, T_)) * 18, 0ull);
+  if (T_ > 0 && L_ > 0) {
+    if (sort_pending_) {
+      cuda_check(cudaStreamWaitEvent(s, ev_join_, 0), "join sort");
+    } else {
+      launch_sort(s);  // sorted keys of the current batch
+    }
+    std::vector<long long> starts(static_cast<size_t>(T_) + 1);
+    for (int t = 0; t < T_; ++t) starts[t] = htabs_[t].idx_off;
+    starts[T_] = L_;
+    long long* d_starts = nullptr;
+    unsigned long long* d_hist = nullptr;
+    cuda_check(cudaMallocAsync(&d_starts, sizeof(long long) * (T_ + 1), s), "malloc");
+    cuda_check(cudaMallocAsync(&d_hist, sizeof(unsigned long long) * T_ * 18, s), "malloc");
+    cuda_check(cudaMemcpyAsync(d_starts, starts.data(), sizeof(long long) * (T_ + 1), cudaMemcpyHostToDevice, s),
+               "starts H2D");
+    cuda_check(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) * T_ * 18, s), "hist reset");
+    row_count_hist_kernel<<<grid_for(L_, 256), 256, 0, s>>>(skey_, d_starts, T_, L_, d_hist);
+    cuda_check(cudaGetLastError(), "row_count_hist_kernel");
+    cuda_check(cudaMemcpyAsync(hist.data(), d_hist, sizeof(unsigned long long) * T_ * 18, cudaMemcpyDeviceToHost, s),
+               "hist D2H");
+    cuda_check(cudaStreamSynchronize(s), "features sync");
+    cudaFree(d_starts);
+    cudaFree(d_hist);
+    sort_pending_ = false;
+  }
+  for (int t = 0; t < T_; ++t) {
+    double* f = out + (size_t)t * 21;
+    const as_table_spec& sp = specs_[t];
+    f[0] = (double)sp.dim;
+    f[1] = (double)sp.hash_size;
+    f[2] = (double)htabs_[t].n_lookups / (double)B_;  // observed_pooling (tables.hpp:337-342)
+    f[3] = (double)((int64_t)sp.dim * sp.hash_size * sp.bytes_per_param) / (1024.0 * 1024.0 * 1024.0);
+    const double distinct = (double)hist[(size_t)t * 18 + 17];
+    for (int b = 0; b < 17; ++b) f[4 + b] = distinct > 0 ? (double)hist[(size_t)t * 18 + b] / distinct : 0.0;
+  }
+}
+
 void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
   check();
   if (t < 0 || t >= T_) fail(AS_LOOKUP, "as_read_rows: table position " + std::to_string(t) + " out of range");

@@ -35,6 +35,7 @@ class EmbContext {
   void step(float lr, float eps, double* loss_host, cudaStream_t s);
   double measure(int warmup, int measure, int trim, bool flush, float lr, float eps);
 
+  void table_features(double* out, cudaStream_t s);
   void read_rows(int t, const int64_t* rows, int64_t n, float* out);
   void read_momentum(int t, const int64_t* rows, int64_t n, float* out);
   void read_buffer(int what, void* host, int64_t nbytes);

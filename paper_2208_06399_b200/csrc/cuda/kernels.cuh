@@ -711,6 +711,40 @@ __global__ void __launch_bounds__(256) pack_indices_kernel(const long long* __re
   }
 }
 
+// ---- cost-model features from the sorted keys ----------
+// For every segment end of the sorted (row, bag) list: occurrence count of the
+// row = end - lower_bound(row) + 1 within its table, binned like
+// detail::frequency_bin (tables.hpp:317-324): (0,1], (1,2], (2,4], ...,
+// (32768, inf) -> 17 bins. hist[t][17] counts rows per bin, hist[t][17] is
+// unused; distinct[t] counts unique rows.
+__global__ void row_count_hist_kernel(const int* __restrict__ skey, const long long* __restrict__ t_start, int T,
+                                      long long L, unsigned long long* __restrict__ hist) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += (long long)gridDim.x * blockDim.x) {
+    // table of element j: last t with t_start[t] <= j (t_start ascending, T+1 entries)
+    int lo = 0, hi = T;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (t_start[mid] <= j) lo = mid; else hi = mid;
+    }
+    const long long t_hi = t_start[lo + 1];
+    const int k = skey[j];
+    if (j + 1 < t_hi && skey[j + 1] == k) continue;  // not the last occurrence
+    long long a = t_start[lo], b = j;  // first occurrence of k in [a, b]
+    while (a < b) {
+      const long long m = (a + b) >> 1;
+      if (skey[m] < k) a = m + 1; else b = m;
+    }
+    const long long c = j - a + 1;
+    int bin = 0;
+    if (c > 1) {
+      bin = 64 - __clzll((unsigned long long)(c - 1));
+      if (bin > 16) bin = 16;
+    }
+    atomicAdd(hist + (long long)lo * 18 + bin, 1ull);
+    atomicAdd(hist + (long long)lo * 18 + 17, 1ull);
+  }
+}
+
 // ---- K6: counter-hash init (bit-identical to oracle/oracle.c) -------------
 __device__ __forceinline__ unsigned long long dev_splitmix64(unsigned long long x) {
   x += 0x9e3779b97f4a7c15ull;

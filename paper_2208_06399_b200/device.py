@@ -158,6 +158,12 @@ class EmbeddingShard:
         check(lib().as_profile_read(self._h, ms, C.byref(n), int(reset)))
         return dict(zip(self.PHASES, list(ms))), n.value
 
+    def features(self, stream=None) -> np.ndarray:
+        """[n_tables, 21] raw cost-model features (extract_features, tables.hpp:344-386) on the GPU."""
+        out = np.zeros((max(1, len(self.tables)), 21), dtype=np.float64)
+        check(lib().as_table_features(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), _stream(stream)))
+        return out[: len(self.tables)]
+
     # -- introspection / readback -------------------------------------------
     def info(self) -> CtxInfoC:
         i = CtxInfoC()

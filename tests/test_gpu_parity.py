@@ -332,3 +332,39 @@ def test_async_staging_pipeline_matches_sync_load(P, oracle, cuda):
             sh.commit()
         with pytest.raises(P.StateError):
             sh.forward()
+
+
+def _features_np(tab, idx, B):
+    """extract_features raw layout (tables.hpp:344-386), restated with numpy."""
+    f = np.zeros(21)
+    f[0], f[1], f[2] = tab.dim, tab.hash_size, len(idx) / B
+    f[3] = tab.dim * tab.hash_size * tab.bytes_per_param / 1024.0 ** 3
+    if len(idx):
+        _, counts = np.unique(idx, return_counts=True)
+        bins = np.zeros(17)
+        for c in counts:
+            b = 0 if c <= 1 else min(int(c - 1).bit_length(), 16)
+            bins[b] += 1
+        f[4:] = bins / len(counts)
+    return f
+
+
+def test_gpu_cost_model_features(P, cuda):
+    """the 21 raw features of extract_features from the GPU sort,
+    exact (integer bins, same division) — including a hot row > 32768 hits."""
+    pool = P.generate_pool(0, 12, P.GeneratorConfig(hash_size_max=3e5, pooling_mean_target=30.0))
+    B = 4096
+    wl = P.generate_workload(0, pool, B)
+    st = streams_of(wl, pool)
+    extra = P.TableDesc(id=99, dim=16, hash_size=50, pooling_mean=20.0)
+    off = np.arange(B + 1, dtype=np.int64) * 20
+    idx = np.zeros(B * 20, dtype=np.int64)
+    idx[::7] = 3
+    tables, streams = pool + [extra], st + [(off, idx)]
+    with P.EmbeddingShard(tables, B) as sh:
+        sh.load(streams)
+        got = sh.features()
+        want = np.stack([_features_np(t, s[1], B) for t, s in zip(tables, streams)])
+        assert np.array_equal(got, want)
+        sh.forward()  # with the side-stream sort in flight
+        assert np.array_equal(sh.features(), want)

@@ -164,3 +164,21 @@ def test_cpu_step_port_matches_f64_oracle(oracle):
         Wt = W[off_w:off_w + t.hash_size * t.dim].reshape(t.hash_size, t.dim)
         assert np.allclose(Wt[r["rows"]], r["w"], rtol=1e-5, atol=1e-6)
         off_w += t.hash_size * t.dim
+
+
+def test_features_numpy_restatement_matches_reference(ref):
+    """Pins the numpy extract_features restatement used by the GPU feature
+    test against the reference's own extract_features (tables.hpp:344-386)."""
+    import ctypes as C
+
+    from test_gpu_parity import _features_np
+
+    pool = ref.generate_pool(0, 6, pooling_mean_target=25.0, hash_size_max=2e4)
+    h, w = ref.generate_workload(0, pool, 1024)
+    out = (C.c_double * (21 * len(pool)))()
+    rc = ref.lib.ref_extract_features(__import__("oracle").tables_to_c(pool), len(pool), h, out)
+    ref.free_workload(h)
+    assert rc == 0
+    got = np.array(list(out)).reshape(len(pool), 21)
+    want = np.stack([_features_np(t, w[t.id][1], 1024) for t in pool])
+    assert np.array_equal(got, want)
