@@ -50,14 +50,26 @@ struct DeviceGuard {
   }
 };
 
-int kind_for_dim(int dim) {
+// Lane layout of a table: NV = vec float4 per lane when the row is wide enough
+// for >= 8 lanes (one warp instruction then gathers 32/GL rows), else 1.
+int kind_for_dim(int dim, int vec) {
   const int nvec = dim / 4;
-  if (nvec <= 1) return 0;
-  if (nvec <= 2) return 1;
-  if (nvec <= 4) return 2;
-  if (nvec <= 8) return 3;
-  if (nvec <= 16) return 4;
-  if (nvec <= 32) return 5;
+  auto pow2ceil = [](int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+  };
+  if (vec >= 2 && nvec >= 16 && nvec <= 32 * vec) {
+    const int nv = (vec >= 4 && nvec >= 32) ? 4 : 2;
+    const int gl = std::min(32, pow2ceil((nvec + nv - 1) / nv));
+    for (int k = 0; k < kNumKinds; ++k)
+      if (kind_gl(k) == gl && kind_nv(k) == nv) return k;
+  }
+  if (nvec <= 32) {
+    const int gl = pow2ceil(std::max(1, nvec));
+    for (int k = 0; k <= 5; ++k)
+      if (kind_gl(k) == gl) return k;
+  }
   if (nvec <= 64) return 6;
   if (nvec <= 128) return 7;
   return 8;
@@ -176,6 +188,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   if (device < 0 || device >= ndev)
     fail(AS_CONFIG, "as_create: device " + std::to_string(device) + " out of range (" +
                         std::to_string(ndev) + " visible)");
+  if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
   specs_.assign(tables, tables + n);
   htabs_.resize(static_cast<size_t>(n));
   int64_t w_off = 0;
@@ -193,7 +206,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     d.dim = s.dim;
     d.col = static_cast<int>(sum_dim_);
     d.table_id = s.id;
-    d.kind = kind_for_dim(s.dim);
+    d.kind = kind_for_dim(s.dim, vec_);
     d.chunk_len = chunk_len_for(s.dim, 131072.0);
     total_rows_ += s.hash_size;
     w_off += s.hash_size * s.dim;
@@ -421,7 +434,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
     DevTable& d = sl.tabs[t];
     d.chunk_len = chunk_len_for(specs_[t].dim, target);
-    const int R = 32 >> std::min(d.kind, 5);
+    const int R = 32 / kind_gl(d.kind);
     const int64_t chunks = (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
     const int64_t units = (chunks + R - 1) / R;
     units_of[t] = units;
@@ -435,14 +448,14 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   // warp units: tables on the TMA path (rows >= 100 floats) first, one launch each
   for (int pass = 0; pass < 2; ++pass)
     for (int t = 0; t < T_; ++t) {
-      const bool tma = use_tma_ && sl.tabs[t].kind >= 5;
+      const bool tma = use_tma_ && kind_gl(sl.tabs[t].kind) == 32;
       if (tma != (pass == 0)) continue;
       sl.tabs[t].unit_off = static_cast<int>(nun);
       nun += units_of[t];
     }
   sl.n_tma_units = 0;
   for (int t = 0; t < T_; ++t)
-    if (use_tma_ && sl.tabs[t].kind >= 5) sl.n_tma_units += units_of[t];
+    if (use_tma_ && kind_gl(sl.tabs[t].kind) == 32) sl.n_tma_units += units_of[t];
   if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
   if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
   sl.L = L;

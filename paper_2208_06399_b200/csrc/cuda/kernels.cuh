@@ -201,15 +201,17 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
 
 // Staged ints per warp and buffer for lane layout `kind`: row ids R*SR, keys R*(SR+1).
-__host__ __device__ constexpr int stage_x_ints(int kind) {
-  return kind <= 1 ? 256 : (kind <= 5 ? (32 >> kind) * 32 : 32);
-}
-__host__ __device__ constexpr int stage_s_ints(int kind) {
-  return kind == 0 ? 288 : (kind == 1 ? 272 : (kind <= 5 ? (32 >> kind) * 33 : 33));
-}
+__host__ __device__ constexpr int stage_sr(int kind) { return 8 * kind_gl(kind) < 32 ? 8 * kind_gl(kind) : 32; }
+__host__ __device__ constexpr int stage_x_ints(int kind) { return (32 / kind_gl(kind)) * stage_sr(kind); }
+__host__ __device__ constexpr int stage_s_ints(int kind) { return (32 / kind_gl(kind)) * (stage_sr(kind) + 1); }
 
 // EXACT: dim == 4*GL*NV, so every lane owns a full column slice and the gathers
 // need no column predicate.
+#ifdef ASB_ABLATE_GATHER  // ablation builds only: every gather hits row 0 (L1-resident)
+#define ASB_ROWID(x) (0u * (unsigned)(x))
+#else
+#define ASB_ROWID(x) ((unsigned)(x))
+#endif
 template <bool FWD, int GL, int NV, bool EXACT>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
   const int kStageX = p.stage_x, kStageS = p.stage_s;
@@ -305,7 +307,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
       if (m0 + U <= nval) {  // full batch: no element predicate
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const char* row = gbase + (size_t)(unsigned)gx[m0 + u] * gstride;
+          const char* row = gbase + (size_t)ASB_ROWID(gx[m0 + u]) * gstride;
 #pragma unroll
           for (int w = 0; w < NV; ++w)
             v[u][w] = (EXACT || c + w * GL < nvec) ? ldg4(reinterpret_cast<const float*>(row + w * GL * 16))
@@ -315,7 +317,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool ok = m0 + u < nval;
-          const char* row = gbase + (size_t)(unsigned)gx[m0 + u] * gstride;
+          const char* row = gbase + (size_t)ASB_ROWID(gx[m0 + u]) * gstride;
 #pragma unroll
           for (int w = 0; w < NV; ++w)
             v[u][w] = (ok && (EXACT || c + w * GL < nvec))
@@ -384,7 +386,12 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             } else if constexpr (FWD) {
               store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
             } else {
+#ifdef ASB_ABLATE_EPILOGUE  // ablation builds only: write g, skip the row update
+              if (c == 0) p.M[s] = acc[0].x;
+              if (false) {
+#else
               if (s == spre) {
+#endif
                 adagrad_row<GL, NV>(p, tb, gmask, s, acc, c, wpre, mpre);
               } else {
                 float4 wr[NV];
@@ -435,23 +442,27 @@ __global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegP
   int* x = seg_smem + warp * 2 * (p.stage_x + p.stage_s);
   int* s = x + 2 * p.stage_x;
   // lane layouts; "exact" widths (dim = 4*GL*NV) drop the column predicate
-  const bool ex = tb.dim == 4 * (tb.kind <= 5 ? (1 << tb.kind) : 32) * (tb.kind <= 5 ? 1 : 1 << (tb.kind - 5));
-#define ASB_SEG_CASE(K, GLV, NVV)                                    \
-  case K:                                                            \
-    if (ex)                                                          \
-      seg_unit<FWD, GLV, NVV, true>(p, tb, t, unit, x, s);           \
-    else                                                             \
-      seg_unit<FWD, GLV, NVV, false>(p, tb, t, unit, x, s);          \
+  const bool ex = tb.dim == 4 * kind_gl(tb.kind) * kind_nv(tb.kind);
+#define ASB_SEG_CASE(K)                                                                  \
+  case K:                                                                                \
+    if (ex)                                                                              \
+      seg_unit<FWD, kind_gl(K), kind_nv(K), true>(p, tb, t, unit, x, s);                 \
+    else                                                                                 \
+      seg_unit<FWD, kind_gl(K), kind_nv(K), false>(p, tb, t, unit, x, s);                \
     break;
   switch (tb.kind) {
-    ASB_SEG_CASE(0, 1, 1)
-    ASB_SEG_CASE(1, 2, 1)
-    ASB_SEG_CASE(2, 4, 1)
-    ASB_SEG_CASE(3, 8, 1)
-    ASB_SEG_CASE(4, 16, 1)
-    ASB_SEG_CASE(5, 32, 1)
-    ASB_SEG_CASE(6, 32, 2)
-    ASB_SEG_CASE(7, 32, 4)
+    ASB_SEG_CASE(0)
+    ASB_SEG_CASE(1)
+    ASB_SEG_CASE(2)
+    ASB_SEG_CASE(3)
+    ASB_SEG_CASE(4)
+    ASB_SEG_CASE(5)
+    ASB_SEG_CASE(6)
+    ASB_SEG_CASE(7)
+    ASB_SEG_CASE(9)
+    ASB_SEG_CASE(10)
+    ASB_SEG_CASE(11)
+    ASB_SEG_CASE(12)
     default:
       if (ex)
         seg_unit<FWD, 32, 8, true>(p, tb, t, unit, x, s);
@@ -654,59 +665,6 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
       const int nvec = tabs[ti].dim >> 2;
       float* row = out + (long long)bi * out_stride + tabs[ti].col;
       for (int cv = lane; cv < nvec; cv += 32) st4_streaming(row + cv * 4, make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-  }
-}
-
-// ---- stream packing / validation (load_workload checks on the device) ----
-// Error key: (table position << 42) | (kind << 40) | entry; the smallest wins.
-// kind 0: offsets[0] != 0, 1: decreasing offset, 2: final offset != count,
-// 3: index out of [0, hash).
-__global__ void pack_offsets_kernel(const long long* __restrict__ off64, int T, int B,
-                                    const DevTable* __restrict__ tabs, int* __restrict__ off32,
-                                    unsigned long long* __restrict__ err) {
-  const long long n = (long long)T * (B + 1);
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(e / (B + 1));
-    const int q = (int)(e - (long long)t * (B + 1));
-    const long long o = off64[e];
-    int kind = -1;
-    if (q == 0) {
-      if (o != 0) kind = 0;
-    } else if (o < off64[e - 1]) {
-      kind = 1;
-    }
-    if (kind < 0 && q == B && o != tabs[t].n_lookups) kind = 2;
-    if (kind >= 0) {
-      atomicMin(err, ((unsigned long long)t << 42) | ((unsigned long long)kind << 40) | (unsigned long long)q);
-    } else if (q < B) {
-      off32[(long long)t * B + q] = (int)(tabs[t].idx_off + o);
-    } else if (t == T - 1) {
-      off32[(long long)T * B] = (int)(tabs[t].idx_off + o);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) pack_indices_kernel(const long long* __restrict__ idx64,
-                                                           const DevTable* __restrict__ tabs,
-                                                           const int* __restrict__ unit_table, int n_units,
-                                                           int* __restrict__ idx32,
-                                                           unsigned long long* __restrict__ err) {
-  const int unit = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (unit >= n_units) return;
-  const int lane = threadIdx.x & 31;
-  const int t = unit_table[unit];
-  const DevTable tb = tabs[t];
-  const long long per = (long long)(32 >> (tb.kind < 5 ? tb.kind : 5)) * tb.chunk_len;
-  const long long j_lo = tb.idx_off + (long long)(unit - tb.unit_off) * per;
-  const long long j_hi = min(j_lo + per, tb.idx_off + tb.n_lookups);
-  for (long long j = j_lo + lane; j < j_hi; j += 32) {
-    const long long v = idx64[j];
-    if (v < 0 || v >= tb.hash) {
-      atomicMin(err, ((unsigned long long)t << 42) | (3ull << 40) | (unsigned long long)(j - tb.idx_off));
-    } else {
-      idx32[j] = (int)(tb.row_off + v);
     }
   }
 }

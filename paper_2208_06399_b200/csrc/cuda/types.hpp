@@ -19,8 +19,17 @@ struct DevTable {
   int unit_off;   // first warp unit; a warp unit = 32/GL consecutive chunks
   int n_units;
   int table_id;
-  int kind;  // lane layout: 0..5 -> GL = 1<<kind, NV = 1; 6,7,8 -> GL = 32, NV = 2,4,8
+  int kind;  // lane layout (GL lanes per row, NV float4 per lane), see kind_gl / kind_nv
 };
+
+// Lane layouts: kinds 0..5: GL = 1..32, NV = 1; 6,7,8: GL = 32, NV = 2,4,8;
+// 9: GL 8 NV 2; 10: GL 16 NV 2; 11: GL 8 NV 4; 12: GL 16 NV 4 (wider per-lane
+// vectors: one warp instruction gathers 2-4 rows).
+__host__ __device__ constexpr int kind_gl(int k) {
+  return k <= 5 ? 1 << k : (k <= 8 ? 32 : ((k == 9 || k == 11) ? 8 : 16));
+}
+__host__ __device__ constexpr int kind_nv(int k) { return k <= 5 ? 1 : (k <= 8 ? 1 << (k - 5) : (k <= 10 ? 2 : 4)); }
+constexpr int kNumKinds = 13;
 
 struct SegParams {
   const DevTable* tabs;
