@@ -36,6 +36,31 @@ __device__ __forceinline__ float4 shfl4_up(float4 v, int d) {
                      __shfl_up_sync(0xffffffffu, v.z, d), __shfl_up_sync(0xffffffffu, v.w, d));
 }
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// L2 eviction priorities (ASB_L2HINTS): gathered rows (re-read ~L/U times)
+// evict_last, the streamed index arrays evict_first.
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 ldg4_hint(const float* p, unsigned long long pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+#ifdef ASB_L2HINTS
+#define ASB_GATHER(ptr) ldg4_hint(ptr, gpol)
+#else
+#define ASB_GATHER(ptr) ldg4(ptr)
+#endif
 __device__ __forceinline__ void st4_streaming(float* p, float4 v) {
   __stcs(reinterpret_cast<float4*>(p), v);
 }
@@ -174,7 +199,13 @@ __device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int w
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+#ifdef ASB_L2HINTS
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem),
+               "l"(l2_policy_first())
+               : "memory");
+#else
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -244,6 +275,9 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     gstride = (unsigned)p.grad_stride * 4u;
   }
   gbase += c * 16;
+#ifdef ASB_L2HINTS
+  const unsigned long long gpol = l2_policy_last();
+#endif
 
   // stage the row ids [base, base+SR) and keys [base, base+SR] of one super-round
   auto stage = [&](long long base, int buf) {
@@ -310,7 +344,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           const char* row = gbase + (size_t)ASB_ROWID(gx[m0 + u]) * gstride;
 #pragma unroll
           for (int w = 0; w < NV; ++w)
-            v[u][w] = (EXACT || c + w * GL < nvec) ? ldg4(reinterpret_cast<const float*>(row + w * GL * 16))
+            v[u][w] = (EXACT || c + w * GL < nvec) ? ASB_GATHER(reinterpret_cast<const float*>(row + w * GL * 16))
                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       } else {
@@ -321,7 +355,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
           for (int w = 0; w < NV; ++w)
             v[u][w] = (ok && (EXACT || c + w * GL < nvec))
-                          ? ldg4(reinterpret_cast<const float*>(row + w * GL * 16))
+                          ? ASB_GATHER(reinterpret_cast<const float*>(row + w * GL * 16))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
