@@ -484,6 +484,13 @@ __global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegP
     else                                                                                 \
       seg_unit<FWD, kind_gl(K), kind_nv(K), false>(p, tb, t, unit, x, s);                \
     break;
+#ifdef ASB_ONLY_KIND  // register/spill study builds only
+  switch (ASB_ONLY_KIND) {
+    ASB_SEG_CASE(ASB_ONLY_KIND)
+    default: break;
+  }
+  return;
+#endif
   switch (tb.kind) {
     ASB_SEG_CASE(0)
     ASB_SEG_CASE(1)
