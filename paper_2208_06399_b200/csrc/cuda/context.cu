@@ -218,6 +218,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     stage_x_ = std::max(stage_x_, stage_x_ints(htabs_[t].kind));
     stage_s_ = std::max(stage_s_, stage_s_ints(htabs_[t].kind));
   }
+  stage_s_ = (stage_s_ + 3) & ~3;  // 16-B aligned id buffers (vector LDS of row ids)
   seg_smem_bytes_ = static_cast<size_t>(kSegWarps) * 2 * (stage_x_ + stage_s_) * sizeof(int);
   if (total_rows_ >= (1LL << 31))
     fail(AS_SHAPE, "as_create: a shard holds at most 2^31-1 rows (int32 row ids), got " +
@@ -239,6 +240,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
+  cuda_check(cudaHostAlloc(&h_loss_, sizeof(double), cudaHostAllocDefault), "pinned loss");
   counters_ = static_cast<int*>(dalloc(sizeof(int) * 4));
   int sms = 148;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
@@ -252,7 +254,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   // Index staging is small: carve out just enough shared memory for the
   // resident CTAs and leave the rest of the unified 228 KB to L1 (hot rows).
   {
-    const double need = (double)ASB_SEG_MINBLOCKS * (double)(seg_smem_bytes_ + 1024);
+    const double need = (double)std::max(ASB_SEG_MINBLOCKS_FWD, ASB_SEG_MINBLOCKS_BWD) * (double)(seg_smem_bytes_ + 1024);
     const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)) + 1);
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
@@ -309,6 +311,7 @@ EmbContext::~EmbContext() {
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
   if (ev_done_) cudaEventDestroy(ev_done_);
+  if (h_loss_) cudaFreeHost(h_loss_);
   if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -750,10 +753,13 @@ void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
   forward(out_, loss_host ? loss_ : nullptr, s);
   backward(out_, lr, eps, s);
   if (loss_host) {
-    cuda_check(cudaMemcpyAsync(loss_host, loss_, sizeof(double), cudaMemcpyDeviceToHost, s), "loss D2H");
-    // sleep (not spin) until the step is done: the staging pool needs the cores
+    // D2H into pinned memory, then sleep (not spin) until the step is done: a
+    // pageable D2H would hold the driver inside the copy for the whole step and
+    // stall the staging threads' H2D submissions; the pool also needs the cores
+    cuda_check(cudaMemcpyAsync(h_loss_, loss_, sizeof(double), cudaMemcpyDeviceToHost, s), "loss D2H");
     cuda_check(cudaEventRecord(ev_done_, s), "done");
     cuda_check(cudaEventSynchronize(ev_done_), "step sync");
+    *loss_host = *h_loss_;
     check();  // report a bad batch with the step's result
   }
 }

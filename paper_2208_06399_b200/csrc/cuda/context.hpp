@@ -102,6 +102,7 @@ class EmbContext {
   cudaStream_t copy_ = nullptr;
   unsigned long long* err_ = nullptr;
   double* loss_ = nullptr;
+  double* h_loss_ = nullptr;  // pinned: a pageable D2H would block every other thread's CUDA calls
   void* flush_ = nullptr;
   size_t flush_bytes_ = 0;
 

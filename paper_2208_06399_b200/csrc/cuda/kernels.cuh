@@ -23,8 +23,54 @@
 
 namespace asb {
 
+// Packed fp32 pair add (FADD2 on sm_100a): IEEE round-to-nearest per element,
+// bit-identical to two FADDs, half the issue slots.
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  float2 r;
+  asm("{\n.reg .b64 a, b, d;\n"
+      "mov.b64 a, {%2, %3};\n"
+      "mov.b64 b, {%4, %5};\n"
+      "add.rn.f32x2 d, a, b;\n"
+      "mov.b64 {%0, %1}, d;\n}\n"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+#ifdef ASB_NO_FADD2
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+#else
+  const float2 lo = f2add(make_float2(a.x, a.y), make_float2(b.x, b.y));
+  const float2 hi = f2add(make_float2(a.z, a.w), make_float2(b.z, b.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+#endif
+}
+// base + row * stride in ONE IMAD.WIDE.U32 (64-bit addend)
+__device__ __forceinline__ const char* row_addr(const char* base, unsigned row, unsigned stride) {
+  const char* r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(row), "r"(stride), "l"(base));
+  return r;
+}
+// U consecutive staged row ids (16-B aligned when U % 4 == 0) with vector LDS
+template <int U>
+__device__ __forceinline__ void lds_ids(const int* p, int (&x)[U]) {
+  if constexpr (U % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < U / 4; ++i) {
+      const int4 v = reinterpret_cast<const int4*>(p)[i];
+      x[4 * i] = v.x;
+      x[4 * i + 1] = v.y;
+      x[4 * i + 2] = v.z;
+      x[4 * i + 3] = v.w;
+    }
+  } else if constexpr (U == 2) {
+    const int2 v = *reinterpret_cast<const int2*>(p);
+    x[0] = v.x;
+    x[1] = v.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < U; ++i) x[i] = p[i];
+  }
 }
 __device__ __forceinline__ float f4dot(float4 a) { return a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w; }
 __device__ __forceinline__ float4 shfl4(float4 v, int src) {
@@ -338,10 +384,12 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     for (int m0 = 0; m0 < SR; m0 += U) {
       unsigned ebits = (endm >> m0) & low_bits<U>();
       float4 v[U][NV];
+      int ids[U];
+      lds_ids<U>(gx + m0, ids);
       if (m0 + U <= nval) {  // full batch: no element predicate
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const char* row = gbase + (size_t)ASB_ROWID(gx[m0 + u]) * gstride;
+          const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
           for (int w = 0; w < NV; ++w)
             v[u][w] = (EXACT || c + w * GL < nvec) ? ASB_GATHER(reinterpret_cast<const float*>(row + w * GL * 16))
@@ -351,7 +399,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool ok = m0 + u < nval;
-          const char* row = gbase + (size_t)ASB_ROWID(gx[m0 + u]) * gstride;
+          const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
           for (int w = 0; w < NV; ++w)
             v[u][w] = (ok && (EXACT || c + w * GL < nvec))
@@ -460,11 +508,18 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   }
 }
 
-template <bool FWD>
 #ifndef ASB_SEG_MINBLOCKS
 #define ASB_SEG_MINBLOCKS 4
 #endif
-__global__ void __launch_bounds__(256, ASB_SEG_MINBLOCKS) seg_reduce_kernel(SegParams p) {
+#ifndef ASB_SEG_MINBLOCKS_FWD
+#define ASB_SEG_MINBLOCKS_FWD ASB_SEG_MINBLOCKS
+#endif
+#ifndef ASB_SEG_MINBLOCKS_BWD
+#define ASB_SEG_MINBLOCKS_BWD ASB_SEG_MINBLOCKS
+#endif
+template <bool FWD>
+__global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MINBLOCKS_BWD)
+    seg_reduce_kernel(SegParams p) {
   // per warp: [2][stage_x] row ids then [2][stage_s] keys (sized on the host
   // for the widest lane layout present in the shard)
   extern __shared__ int seg_smem[];
