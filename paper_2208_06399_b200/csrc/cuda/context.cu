@@ -189,6 +189,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     fail(AS_CONFIG, "as_create: device " + std::to_string(device) + " out of range (" +
                         std::to_string(ndev) + " visible)");
   if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("ASB_CHUNK_KB")) chunk_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
   specs_.assign(tables, tables + n);
   htabs_.resize(static_cast<size_t>(n));
   int64_t w_off = 0;
@@ -429,7 +430,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   // batches so that there is at least about one wave of warps.
   double gbytes = 0.0;
   for (int t = 0; t < T_; ++t) gbytes += 4.0 * specs_[t].dim * (double)std::max<int64_t>(n_idx[t], 0);
-  const double target = std::max(2048.0, std::min(131072.0, gbytes / (148.0 * 24.0)));
+  const double target = std::max(2048.0, std::min(chunk_cap_, gbytes / (148.0 * 24.0)));
   sl.tabs = htabs_;
   int64_t L = 0, nch = 0, nun = 0;
   std::vector<int64_t> units_of(static_cast<size_t>(T_));

@@ -122,6 +122,7 @@ class EmbContext {
   int64_t n_units_ = 0;
   int64_t n_tma_units_ = 0;
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
+  double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
   bool use_tma_ = false;  // ASB_TMA=1: TMA bulk-copy gathers for wide rows (measured 3x slower)
   float* carry_ = nullptr;
   void* cub_tmp_ = nullptr;

@@ -732,7 +732,10 @@ __global__ void __launch_bounds__(256) seg_fixup_long_kernel(SegParams p) {
 
 // K4: bag id per lookup from the offsets; empty bags get a zero pooled row
 // here (they have no elements for the segmented reduce). One warp per 32
-// consecutive (table, bag) pairs.
+// consecutive (table, bag) pairs: lane i holds bag i's end offset, and the
+// warp walks the bags' element range 32 elements at a time, each lane finding
+// its element's bag with a 5-step shuffle binary search over the lanes' ends
+// (coalesced stores; no per-bag serial loop).
 __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__ off, int T, int B,
                                                          const DevTable* __restrict__ tabs,
                                                          int* __restrict__ bag, float* __restrict__ out,
@@ -741,27 +744,34 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
   const long long w0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
   if (w0 >= nb) return;
   const int lane = threadIdx.x & 31;
-  const long long gb = w0 + lane;
-  int o = 0, len = 0, b = 0, t = 0;
-  if (gb < nb) {
-    o = __ldg(off + gb);
-    len = __ldg(off + gb + 1) - o;
-    t = (int)(gb / B);
-    b = (int)(gb - (long long)t * B);
-  }
-  const int n = (int)min(32LL, nb - w0);
-  for (int i = 0; i < n; ++i) {
-    const int li = __shfl_sync(0xffffffffu, len, i);
-    const int oi = __shfl_sync(0xffffffffu, o, i);
-    const int bi = __shfl_sync(0xffffffffu, b, i);
-    if (li > 0) {
-      for (int k = lane; k < li; k += 32) bag[oi + k] = bi;
-    } else {
-      const int ti = __shfl_sync(0xffffffffu, t, i);
-      const int nvec = tabs[ti].dim >> 2;
-      float* row = out + (long long)bi * out_stride + tabs[ti].col;
-      for (int cv = lane; cv < nvec; cv += 32) st4_streaming(row + cv * 4, make_float4(0.f, 0.f, 0.f, 0.f));
+  const long long gb = min(w0 + lane, nb - 1);  // lanes past the end repeat the last bag
+  const int o = __ldg(off + gb);
+  const int e = __ldg(off + gb + 1);
+  const int t = (int)(gb / B);
+  const int b = (int)(gb - (long long)t * B);
+  const int first = __shfl_sync(0xffffffffu, o, 0);
+  const int last = __shfl_sync(0xffffffffu, e, 31);
+  for (int base = first; base < last; base += 32) {
+    const int j = base + lane;
+    // number of lanes whose bag ends at or before j = j's bag (ends ascending)
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int v = __shfl_sync(0xffffffffu, e, lo + step - 1);
+      if (v <= j) lo += step;
     }
+    const int bj = __shfl_sync(0xffffffffu, b, lo);
+    if (j < last) bag[j] = bj;
+  }
+  unsigned empty = __ballot_sync(0xffffffffu, w0 + lane < nb && o == e);
+  while (empty) {
+    const int i = __ffs(empty) - 1;
+    empty &= empty - 1;
+    const int ti = __shfl_sync(0xffffffffu, t, i);
+    const int bi = __shfl_sync(0xffffffffu, b, i);
+    const int nvec = tabs[ti].dim >> 2;
+    float* row = out + (long long)bi * out_stride + tabs[ti].col;
+    for (int cv = lane; cv < nvec; cv += 32) st4_streaming(row + cv * 4, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 
