@@ -5,10 +5,10 @@
 // HBM layout (per context):
 //   W      fp32, tables concatenated in context order, each [hash_t, dim_t] row-major
 //   M      fp32 [sum hash_t]  row-wise Adagrad momentum, indexed by GLOBAL row
-//   idx32  int32 [L]  lookups as GLOBAL rows (row_off_t + idx), table-major
+//   idx32  int32 [L]  lookups as table-local rows, table-major
 //   off32  int32 [T*B + 1] rebased bag offsets (TBE layout)
 //   bag    int32 [L]  bag id of each lookup (K4)
-//   skey/sbag int32 [L] lookups sorted by global row (stable), with bag ids
+//   skey/sbag int32 [L] each table's lookups sorted by row (stable), with bag ids
 //   pooled fp32 [B, sum dim_t], table columns in context order
 #include "context.hpp"
 #include "kernels.cuh"
@@ -202,7 +202,8 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     DevTable& d = htabs_[t];
     std::memset(&d, 0, sizeof d);
     d.row_off = total_rows_;
-    d.w_base = w_off - total_rows_ * s.dim;
+    d.w_base = w_off;
+    d.sort_bits = std::max(1, bit_width_u64(static_cast<uint64_t>(s.hash_size - 1)));
     d.hash = s.hash_size;
     d.dim = s.dim;
     d.col = static_cast<int>(sum_dim_);
@@ -221,10 +222,10 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   }
   stage_s_ = (stage_s_ + 3) & ~3;  // 16-B aligned id buffers (vector LDS of row ids)
   seg_smem_bytes_ = static_cast<size_t>(kSegWarps) * 2 * (stage_x_ + stage_s_) * sizeof(int);
-  if (total_rows_ >= (1LL << 31))
-    fail(AS_SHAPE, "as_create: a shard holds at most 2^31-1 rows (int32 row ids), got " +
-                       std::to_string(total_rows_));
-  end_bit_ = std::max(1, bit_width_u64(static_cast<uint64_t>(std::max<int64_t>(total_rows_ - 1, 0))));
+  for (int t = 0; t < n; ++t)
+    if (specs_[t].hash_size >= (1LL << 31))
+      fail(AS_SHAPE, "table " + std::to_string(specs_[t].id) + ": at most 2^31-1 rows (int32 row ids), got " +
+                         std::to_string(specs_[t].hash_size));
 
   DeviceGuard g(device_);
   dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
@@ -325,17 +326,23 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
   };
   if (L > cap_L_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
-    for (void* p : {(void*)bag_, (void*)skey_, (void*)sbag_, cub_tmp_}) drop(p);
+    for (void* p : {(void*)bag_, (void*)skey_, (void*)sbag_, (void*)tkey_, (void*)tbag_}) drop(p);
     const int64_t cap = std::max<int64_t>(L + L / 8, 1024);
     bag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     skey_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     sbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
-    size_t tmp = 0;
-    cuda_check(sort_pairs(nullptr, tmp, nullptr, nullptr, nullptr, nullptr, (int)cap, end_bit_, nullptr),
-               "sort sizing");
-    cub_bytes_ = tmp;
-    cub_tmp_ = dalloc(tmp);
+    tkey_ = static_cast<int*>(dalloc(sizeof(int) * cap));
+    tbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     cap_L_ = cap;
+  }
+  // K2 scratch: [T][4][256] digit bins | [4][T] + [4] tile counters | [4][tiles][256] look-back
+  const int64_t tiles = (L + kSortTile - 1) / kSortTile + T_;
+  if (tiles > cap_sort_tiles_) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    drop(sort_scratch_);
+    const int64_t cap = tiles + tiles / 8 + 16;
+    sort_scratch_ = static_cast<int*>(dalloc(sizeof(int) * (sort_fixed_ints() + kMaxSortPasses * cap * kSortDigits)));
+    cap_sort_tiles_ = cap;
   }
   if (n_chunks > cap_chunks_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
@@ -465,6 +472,44 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   sl.L = L;
   sl.nch = nch;
   sl.nun = nun;
+  // K2 layout: sort tiles per table, tables taking part in each digit pass
+  // (their tile prefix) and the histogram CTAs
+  {
+    // meta: [hist CTA -> table][hist CTA -> chunk in table][pass p: tile -> table]...
+    int64_t tiles = 0, hctas = 0;
+    int pmax = 0;
+    std::vector<int64_t> tiles_of(static_cast<size_t>(T_));
+    for (int t = 0; t < T_; ++t) {
+      if (n_idx[t] >= (1LL << 30))
+        fail(AS_SHAPE, "table " + std::to_string(specs_[t].id) + ": at most 2^30-1 lookups per batch");
+      tiles_of[t] = (n_idx[t] + kSortTile - 1) / kSortTile;
+      sl.tabs[t].sort_tile_off = static_cast<int>(tiles);
+      tiles += tiles_of[t];
+      hctas += (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta;
+      if (n_idx[t] > 0) pmax = std::max(pmax, sort_passes_of(sl.tabs[t].sort_bits));
+    }
+    std::vector<int>& m = sl.sort_meta;
+    m.clear();
+    m.reserve(static_cast<size_t>(2 * hctas + pmax * tiles));
+    for (int t = 0; t < T_; ++t)
+      for (int64_t k = 0; k < (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta; ++k) m.push_back(t);
+    for (int t = 0; t < T_; ++t)
+      for (int64_t k = 0; k < (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta; ++k) m.push_back((int)k);
+    for (int p = 0; p < kMaxSortPasses; ++p) {
+      sl.tile_tab_off[p] = static_cast<int64_t>(m.size());
+      int64_t acc = 0;
+      if (p < pmax)
+        for (int t = 0; t < T_; ++t)
+          if (n_idx[t] > 0 && sort_passes_of(sl.tabs[t].sort_bits) > p) {
+            m.insert(m.end(), static_cast<size_t>(tiles_of[t]), t);
+            acc += tiles_of[t];
+          }
+      sl.pass_tiles[p] = acc;
+    }
+    sl.n_sort_tiles = tiles;
+    sl.n_hist_ctas = hctas;
+    sl.sort_passes = pmax;
+  }
   sl.utab.assign(static_cast<size_t>(nun), 0);
   for (int t = 0; t < T_; ++t)
     std::fill(sl.utab.begin() + sl.tabs[t].unit_off, sl.utab.begin() + sl.tabs[t].unit_off + sl.tabs[t].n_units, t);
@@ -534,7 +579,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
           const int64_t* src = idx[t];
           int* dst = sp->h_idx32 + d.idx_off;
           const int64_t hash = d.hash;
-          const bool bad = narrow_rows(src + b, dst + b, e - b, hash, (int)d.row_off);
+          const bool bad = narrow_rows(src + b, dst + b, e - b, hash, 0);
           if (bad)
             for (int64_t j = b; j < e; ++j)
               if (src[j] < 0 || src[j] >= hash) {
@@ -600,6 +645,27 @@ void EmbContext::commit(cudaStream_t s) {
   if (sl.nun > 0)
     cuda_check(cudaMemcpyAsync(unit_table_, sl.utab.data(), sizeof(int) * sl.nun, cudaMemcpyHostToDevice, s),
                "unit table H2D");
+  if ((int64_t)sl.sort_meta.size() > cap_sort_meta_) {
+    cuda_check(cudaStreamSynchronize(s), "grow sync");
+    if (sort_meta_) {
+      auto it = std::find(allocs_.begin(), allocs_.end(), (void*)sort_meta_);
+      if (it != allocs_.end()) allocs_.erase(it);
+      cudaFree(sort_meta_);
+    }
+    cap_sort_meta_ = (int64_t)sl.sort_meta.size() + (int64_t)sl.sort_meta.size() / 8 + 64;
+    sort_meta_ = static_cast<int*>(dalloc(sizeof(int) * cap_sort_meta_));
+  }
+  if (!sl.sort_meta.empty())
+    cuda_check(cudaMemcpyAsync(sort_meta_, sl.sort_meta.data(), sizeof(int) * sl.sort_meta.size(),
+                               cudaMemcpyHostToDevice, s),
+               "sort layout H2D");
+  for (int p = 0; p < kMaxSortPasses; ++p) {
+    tile_tab_off_[p] = sl.tile_tab_off[p];
+    pass_tiles_[p] = sl.pass_tiles[p];
+  }
+  n_sort_tiles_ = sl.n_sort_tiles;
+  n_hist_ctas_ = sl.n_hist_ctas;
+  sort_passes_ = sl.sort_passes;
   idx32_ = sl.d_idx32;
   off32_ = sl.d_off32;
   cur_slot_ = (int)(&sl - slots_);
@@ -702,18 +768,41 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   launches_ += 3;
 }
 
-// K2: stable radix sort of (global row, bag) pairs. Depends only on the
-// loaded batch and the bag ids of K4, so as_forward launches it on a side
-// stream right after K4 where it overlaps the forward gather; the backward
-// joins on it (or sorts inline when no forward ran since the load).
+// K2: stable radix sort of each table's (row, bag) pairs (sort.cuh). Depends
+// only on the loaded batch and the bag ids of K4, so as_forward launches it on
+// a side stream right after K4 where it overlaps the forward gather; the
+// backward joins on it (or sorts inline when no forward ran since the load).
 void EmbContext::launch_sort(cudaStream_t s) {
-  size_t tmp = cub_bytes_;
   Phase ph(this, 3, s);
-  cuda_check(sort_pairs(cub_tmp_, tmp, reinterpret_cast<const unsigned*>(idx32_), reinterpret_cast<unsigned*>(skey_),
-                        bag_, sbag_, (int)L_, end_bit_, s),
-             "radix sort");
-  // onesweep: histogram + exclusive-sum + one pass per digit
-  launches_ += 2 + sort_passes(end_bit_);
+  if (sort_passes_ == 0) return;
+  SortParams sp;
+  std::memset(&sp, 0, sizeof sp);
+  sp.tabs = dtabs_;
+  sp.T = T_;
+  sp.keys_in = reinterpret_cast<const unsigned*>(idx32_);
+  sp.vals_in = bag_;
+  sp.keys_out = reinterpret_cast<unsigned*>(skey_);
+  sp.vals_out = sbag_;
+  sp.keys_tmp = reinterpret_cast<unsigned*>(tkey_);
+  sp.vals_tmp = tbag_;
+  sp.bins = sort_scratch_;
+  sp.ctrs = sp.bins + (int64_t)T_ * kMaxSortPasses * kSortDigits;
+  sp.lookback = sp.ctrs + kMaxSortPasses * T_ + kMaxSortPasses;
+  sp.n_tiles = (int)n_sort_tiles_;
+  sp.hist_tab = sort_meta_;
+  sp.hist_chunk = sort_meta_ + n_hist_ctas_;
+  for (int p = 0; p < kMaxSortPasses; ++p) sp.tile_tab[p] = sort_meta_ + tile_tab_off_[p];
+  const size_t zero = sizeof(int) * (sort_fixed_ints() + (size_t)sort_passes_ * n_sort_tiles_ * kSortDigits);
+  cuda_check(cudaMemsetAsync(sort_scratch_, 0, zero, s), "sort scratch reset");
+  sort_hist_kernel<<<(unsigned)n_hist_ctas_, kHistThreads, 0, s>>>(sp);
+  cuda_check(cudaGetLastError(), "sort_hist_kernel");
+  sort_scan_kernel<<<dim3((unsigned)T_, (unsigned)sort_passes_), kSortDigits, 0, s>>>(sp);
+  cuda_check(cudaGetLastError(), "sort_scan_kernel");
+  for (int p = 0; p < sort_passes_; ++p) {
+    sort_onesweep_kernel<<<(unsigned)pass_tiles_[p], kSortThreads, 0, s>>>(sp, p);
+    cuda_check(cudaGetLastError(), "sort_onesweep_kernel");
+  }
+  launches_ += 2 + sort_passes_;
 }
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
@@ -855,7 +944,7 @@ void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
   cuda_check(cudaMalloc(&drows, sizeof(long long) * n), "malloc");
   cuda_check(cudaMalloc(&dst, sizeof(float) * n * specs_[t].dim), "malloc");
   cuda_check(cudaMemcpy(drows, rows, sizeof(long long) * n, cudaMemcpyHostToDevice), "rows H2D");
-  const long long w_off = htabs_[t].w_base + htabs_[t].row_off * specs_[t].dim;
+  const long long w_off = htabs_[t].w_base;
   gather_rows_kernel<<<grid_for(n * specs_[t].dim, 256), 256>>>(W_, w_off, specs_[t].dim, drows, n, dst);
   cuda_check(cudaGetLastError(), "gather_rows_kernel");
   cuda_check(cudaMemcpy(out, dst, sizeof(float) * n * specs_[t].dim, cudaMemcpyDeviceToHost), "rows D2H");
@@ -895,6 +984,12 @@ void EmbContext::read_buffer(int what, void* host, int64_t nbytes) {
     fail(AS_SHAPE, "as_read_buffer: buffer " + std::to_string(what) + " has " + std::to_string(want) +
                        " bytes, caller passed " + std::to_string(nbytes));
   if (want) cuda_check(cudaMemcpy(host, src, static_cast<size_t>(want), cudaMemcpyDeviceToHost), "read D2H");
+  if (what == 2 || what == 4) {  // device rows are table-local: report GLOBAL rows (row_off_t + r)
+    int* h = static_cast<int*>(host);
+    for (int t = 0; t < T_; ++t)
+      for (int64_t j = htabs_[t].idx_off; j < htabs_[t].idx_off + htabs_[t].n_lookups; ++j)
+        h[j] += static_cast<int>(htabs_[t].row_off);
+  }
 }
 
 void EmbContext::write_table(int t, const float* w, const float* m) {
@@ -902,7 +997,7 @@ void EmbContext::write_table(int t, const float* w, const float* m) {
   DeviceGuard g(device_);
   const size_t rows = static_cast<size_t>(specs_[t].hash_size);
   if (w) {
-    const long long w_off = htabs_[t].w_base + htabs_[t].row_off * specs_[t].dim;
+    const long long w_off = htabs_[t].w_base;
     cuda_check(cudaMemcpy(W_ + w_off, w, sizeof(float) * rows * specs_[t].dim, cudaMemcpyHostToDevice), "W H2D");
   }
   if (m) cuda_check(cudaMemcpy(M_ + htabs_[t].row_off, m, sizeof(float) * rows, cudaMemcpyHostToDevice), "M H2D");
@@ -922,7 +1017,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + sort_passes(end_bit_));
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + sort_passes_);
 }
 
 }  // namespace asb

@@ -71,7 +71,18 @@ class EmbContext {
   int max_dim_ = 4;
   int stage_x_ = 32, stage_s_ = 33;
   size_t seg_smem_bytes_ = 0;
-  int end_bit_ = 1;
+  // K2 (sort.cuh): per-batch layout, uploaded at commit
+  int64_t sort_fixed_ints() const {
+    return (int64_t)T_ * kMaxSortPasses * kSortDigits + kMaxSortPasses * (int64_t)T_ + kMaxSortPasses;
+  }
+  int* sort_meta_ = nullptr;     // device copy of Slot::sort_meta
+  int64_t cap_sort_meta_ = 0;
+  int* sort_scratch_ = nullptr;  // bins | counters | look-back
+  int64_t cap_sort_tiles_ = 0;
+  int64_t tile_tab_off_[kMaxSortPasses] = {0, 0, 0, 0};
+  int64_t pass_tiles_[kMaxSortPasses] = {0, 0, 0, 0};
+  int64_t n_sort_tiles_ = 0, n_hist_ctas_ = 0;
+  int sort_passes_ = 0;
 
   DevTable* dtabs_ = nullptr;
   float* W_ = nullptr;
@@ -87,6 +98,11 @@ class EmbContext {
     std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
     std::vector<int> utab;
     int64_t L = 0, nch = 0, nun = 0, n_tma_units = 0;
+    std::vector<int> sort_meta;  // hist CTA -> table | hist CTA -> chunk | per pass: tile -> table
+    int64_t tile_tab_off[kMaxSortPasses] = {0, 0, 0, 0};
+    int64_t pass_tiles[kMaxSortPasses] = {0, 0, 0, 0};
+    int64_t n_sort_tiles = 0, n_hist_ctas = 0;
+    int sort_passes = 0;
     cudaEvent_t copied = nullptr;   // all H2D of the batch landed
     cudaEvent_t retired = nullptr;  // the device no longer reads the batch
     std::thread job;                // narrow + validate + H2D
@@ -112,6 +128,8 @@ class EmbContext {
   int* bag_ = nullptr;
   int* skey_ = nullptr;
   int* sbag_ = nullptr;
+  int* tkey_ = nullptr;  // K2 ping-pong
+  int* tbag_ = nullptr;
   int* unit_table_ = nullptr;
   int2* completers_ = nullptr;
   int4* completers_long_ = nullptr;
@@ -125,8 +143,6 @@ class EmbContext {
   double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
   bool use_tma_ = false;  // ASB_TMA=1: TMA bulk-copy gathers for wide rows (measured 3x slower)
   float* carry_ = nullptr;
-  void* cub_tmp_ = nullptr;
-  size_t cub_bytes_ = 0;
 
   cudaStream_t side_ = nullptr;  // K2 sort overlapped with the forward
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_done_ = nullptr;

@@ -147,7 +147,7 @@ __device__ __forceinline__ void load_row_state(const SegParams& p, const DevTabl
                                                float4 (&w)[NV], float& m) {
   const int nvec = tb.dim >> 2;
   const float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
-  m = p.M[seg];
+  m = p.M[tb.row_off + seg];
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     const int cv = c + q * GL;
@@ -181,7 +181,7 @@ __device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& 
       *reinterpret_cast<float4*>(wr + cv * 4) = x;
     }
   }
-  if (c == 0) p.M[seg] = m;
+  if (c == 0) p.M[tb.row_off + seg] = m;
 }
 
 // Predicated variant for lane groups that run converged (GL < 32): every lane
@@ -215,7 +215,7 @@ __device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTa
         *reinterpret_cast<float4*>(wr + cv * 4) = x;
       }
     }
-    if (c == 0) p.M[seg] = m;
+    if (c == 0) p.M[tb.row_off + seg] = m;
   }
 }
 
@@ -469,7 +469,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
               store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
             } else {
 #ifdef ASB_ABLATE_EPILOGUE  // ablation builds only: write g, skip the row update
-              if (c == 0) p.M[s] = acc[0].x;
+              if (c == 0) p.M[tb.row_off + s] = acc[0].x;
               if (false) {
 #else
               if (s == spre) {

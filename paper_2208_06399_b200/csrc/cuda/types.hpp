@@ -3,12 +3,28 @@
 
 #include <vector_types.h>
 
+#ifndef ASB_SORT_THREADS
+#define ASB_SORT_THREADS 384
+#endif
+#ifndef ASB_SORT_ITEMS
+#define ASB_SORT_ITEMS 23
+#endif
+
 namespace asb {
+
+// K2 (sort.cuh): 8-bit digits, onesweep tiles of 384 x 23 elements
+constexpr int kSortBits = 8;
+constexpr int kSortDigits = 1 << kSortBits;
+constexpr int kSortThreads = ASB_SORT_THREADS;
+constexpr int kSortTile = ASB_SORT_THREADS * ASB_SORT_ITEMS;
+constexpr int kMaxSortPasses = 4;    // table-local rows < 2^31
+constexpr int kHistTilesPerCta = 8;  // histogram CTA = 8 consecutive sort tiles of one table
+__host__ __device__ constexpr int sort_passes_of(int bits) { return (bits + kSortBits - 1) / kSortBits; }
 
 // Per-table device descriptor (host-built, see context.cu).
 struct DevTable {
-  long long w_base;     // W element offset with row r (GLOBAL row id) at w_base + r*dim
-  long long row_off;    // first global row of the table
+  long long w_base;     // W element offset of the table: row r (table-local) at w_base + r*dim
+  long long row_off;    // first global row of the table (momentum M[row_off + r])
   long long hash;       // rows
   long long idx_off;    // first element of the table in the lookup arrays
   long long n_lookups;  // L_t of the loaded batch
@@ -20,6 +36,8 @@ struct DevTable {
   int n_units;
   int table_id;
   int kind;  // lane layout (GL lanes per row, NV float4 per lane), see kind_gl / kind_nv
+  int sort_bits;      // bits of the largest table-local row id (K2 passes = ceil(sort_bits / 8))
+  int sort_tile_off;  // first K2 tile of the table (its look-back region)
 };
 
 // Lane layouts: kinds 0..5: GL = 1..32, NV = 1; 6,7,8: GL = 32, NV = 2,4,8;
