@@ -190,6 +190,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
                         std::to_string(ndev) + " visible)");
   if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("ASB_CHUNK_KB")) chunk_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
+  if (const char* e = std::getenv("ASB_UNIT_KB")) unit_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
   specs_.assign(tables, tables + n);
   htabs_.resize(static_cast<size_t>(n));
   int64_t w_off = 0;
@@ -243,11 +244,12 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
   cuda_check(cudaHostAlloc(&h_loss_, sizeof(double), cudaHostAllocDefault), "pinned loss");
-  counters_ = static_cast<int*>(dalloc(sizeof(int) * 4));
+  counters_ = static_cast<int*>(dalloc(sizeof(int) * 6));
   int sms = 148;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_), "SM count");
   fixup_grid_ = static_cast<unsigned>(sms * 2);
   fixup_short_grid_ = static_cast<unsigned>(sms * 16);
+  fixup_lane_grid_ = static_cast<unsigned>(sms * 4);
   int l2 = 0;
   cuda_check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_), "L2 size");
   flush_bytes_ = static_cast<size_t>(std::max(l2, 1 << 20)) * 2;
@@ -349,10 +351,12 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
     drop(carry_);
     drop(completers_);
     drop(completers_long_);
+    drop(completers_mid_);
     const int64_t cap = std::max<int64_t>(n_chunks + n_chunks / 8, 64);
     carry_ = static_cast<float*>(dalloc(sizeof(float) * cap * 2 * max_dim_));
     completers_ = static_cast<int2*>(dalloc(sizeof(int2) * cap));
     completers_long_ = static_cast<int4*>(dalloc(sizeof(int4) * cap));
+    completers_mid_ = static_cast<int2*>(dalloc(sizeof(int2) * cap));
     cap_chunks_ = cap;
   }
   if (n_units > cap_units_) {
@@ -444,8 +448,11 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   for (int t = 0; t < T_; ++t) {
     if (n_idx[t] < 0) fail(AS_OFFSET, "table " + std::to_string(specs_[t].id) + ": negative index count");
     DevTable& d = sl.tabs[t];
-    d.chunk_len = chunk_len_for(specs_[t].dim, target);
     const int R = 32 / kind_gl(d.kind);
+    // a warp unit walks R chunks: cap the unit's bytes, not only the chunk's, so
+    // narrow-row tables do not widen the in-flight window (L2 reuse of the
+    // gathered gradient slabs in the backward)
+    d.chunk_len = chunk_len_for(specs_[t].dim, std::min(target, unit_cap_ / R));
     const int64_t chunks = (n_idx[t] + d.chunk_len - 1) / d.chunk_len;
     const int64_t units = (chunks + R - 1) / R;
     units_of[t] = units;
@@ -697,9 +704,11 @@ SegParams EmbContext::seg_params(bool fwd) const {
   p.unit_table = unit_table_;
   p.n_units = static_cast<int>(n_units_);
   p.completers = completers_;
-  p.n_completers = counters_ + (fwd ? 0 : 2);
+  p.n_completers = counters_ + (fwd ? 0 : 3);
+  p.completers_mid = completers_mid_;
+  p.n_completers_mid = counters_ + (fwd ? 2 : 5);
   p.completers_long = completers_long_;
-  p.n_completers_long = counters_ + (fwd ? 1 : 3);
+  p.n_completers_long = counters_ + (fwd ? 1 : 4);
   p.seg = fwd ? bag_ : skey_;
   p.src = fwd ? idx32_ : sbag_;
   p.carry = carry_;
@@ -754,13 +763,14 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.out = target;
   p.out_stride = sum_dim_;
   p.loss = loss_dev;
-  cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 2, s), "counter reset");
+  cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 3, s), "counter reset");
   {
     Phase ph(this, 1, s);
     launch_seg<true>(p, s);
   }
   {
     Phase ph(this, 2, s);
+    seg_fixup_lane_kernel<true><<<fixup_lane_grid_, kBlock, 0, s>>>(p);
     seg_fixup_kernel<true><<<fixup_short_grid_, kBlock, 0, s>>>(p);
     seg_fixup_long_kernel<true><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<fwd>");
@@ -822,18 +832,19 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   p.M = M_;
   p.lr = lr;
   p.eps = eps;
-  cuda_check(cudaMemsetAsync(counters_ + 2, 0, sizeof(int) * 2, s), "counter reset");
+  cuda_check(cudaMemsetAsync(counters_ + 3, 0, sizeof(int) * 3, s), "counter reset");
   {
     Phase ph(this, 4, s);
     launch_seg<false>(p, s);
   }
   {
     Phase ph(this, 5, s);
+    seg_fixup_lane_kernel<false><<<fixup_lane_grid_, kBlock, 0, s>>>(p);
     seg_fixup_kernel<false><<<fixup_short_grid_, kBlock, 0, s>>>(p);
     seg_fixup_long_kernel<false><<<fixup_grid_, kBlock, 0, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_fixup_kernel<bwd>");
   }
-  launches_ += 2;
+  launches_ += 3;
 }
 
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
@@ -1017,7 +1028,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 7 + 2 + sort_passes_);
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 9 + 2 + sort_passes_);
 }
 
 }  // namespace asb

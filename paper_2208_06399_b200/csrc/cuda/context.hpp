@@ -133,14 +133,17 @@ class EmbContext {
   int* unit_table_ = nullptr;
   int2* completers_ = nullptr;
   int4* completers_long_ = nullptr;
-  int* counters_ = nullptr;  // [0,1] fwd completers (short, long), [2,3] bwd
+  int2* completers_mid_ = nullptr;
+  int* counters_ = nullptr;  // [0,1,2] fwd completers (all, long, mid), [3,4,5] bwd
   unsigned fixup_grid_ = 296;
   unsigned fixup_short_grid_ = 2368;
+  unsigned fixup_lane_grid_ = 592;
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
   int64_t n_tma_units_ = 0;
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
   double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
+  double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)
   bool use_tma_ = false;  // ASB_TMA=1: TMA bulk-copy gathers for wide rows (measured 3x slower)
   float* carry_ = nullptr;
 

@@ -617,14 +617,56 @@ __device__ __forceinline__ void fixup_loss(const SegParams& p, float loss_acc, i
   }
 }
 
+// Thread per completer (the common case first): a segment that began in the
+// previous chunk (k0 = k-1) of a table with rows of <= 32 floats is finished
+// by ONE lane — tail[k-1] + head[k], then the epilogue over the row's <= 8
+// float4 — so a warp finishes 32 of them with all their loads in flight.
+// Anything else goes to the warp-per-completer kernel below.
+template <bool FWD>
+__global__ void __launch_bounds__(256, 4) seg_fixup_lane_kernel(SegParams p) {
+  const int n = *p.n_completers;
+  float loss_acc = 0.f;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 ct = p.completers[i];
+    const int chunk = ct.x;
+    const DevTable& tb = p.tabs[ct.y];
+    const int nvec = tb.dim >> 2;
+    const long long t_lo = tb.idx_off;
+    const long long j0 = t_lo + (long long)(chunk - tb.chunk_off) * tb.chunk_len;  // start of chunk k
+    const int first = __ldg(p.seg + j0);
+    const long long jp = j0 - tb.chunk_len;  // start of chunk k-1
+    if (nvec > 8 || (jp != t_lo && __ldg(p.seg + jp - 1) == first)) {
+      p.completers_mid[atomicAdd(p.n_completers_mid, 1)] = ct;
+      continue;
+    }
+    const float* tail = carry_of(p, chunk - 1, chunk - 1);
+    const float* head = carry_of(p, chunk, chunk - 1);
+    float4 v[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
+      v[w] = w < nvec ? f4add(f4add(make_float4(0.f, 0.f, 0.f, 0.f), *reinterpret_cast<const float4*>(tail + 4 * w)),
+                              *reinterpret_cast<const float4*>(head + 4 * w))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (FWD) {
+      store_pooled<1, 8>(p, tb, first, v, 0, loss_acc);
+    } else {
+      float4 w[8];
+      float m_old;
+      load_row_state<1, 8>(p, tb, first, 0, w, m_old);
+      adagrad_row<1, 8>(p, tb, 1u << (threadIdx.x & 31), first, v, 0, w, m_old);
+    }
+  }
+  fixup_loss<FWD>(p, loss_acc, threadIdx.x & 31);
+}
+
 // Warp per completer. Whole-warp lane layout: lane owns float4 columns lane + 32*w.
 template <bool FWD>
 __global__ void __launch_bounds__(256) seg_fixup_kernel(SegParams p) {
   const int lane = threadIdx.x & 31;
-  const int n = *p.n_completers;
+  const int n = *p.n_completers_mid;
   float loss_acc = 0.f;
   for (int i = blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += gridDim.x * 8) {
-    const int2 ct = p.completers[i];
+    const int2 ct = p.completers_mid[i];
     const int chunk = ct.x;
     const DevTable tb = p.tabs[ct.y];
     const int first = __ldg(p.seg + tb.idx_off + (long long)(chunk - tb.chunk_off) * tb.chunk_len);

@@ -78,6 +78,10 @@ struct SegParams {
   // completers of long segments: {chunk, table, k0, key}
   int4* completers_long;
   int* n_completers_long;
+  // completers the per-lane fixup hands to the warp fixup (segment spans > 2
+  // chunks, or rows wider than 32 floats): {chunk, table}
+  int2* completers_mid;
+  int* n_completers_mid;
 };
 
 }  // namespace asb
