@@ -28,7 +28,8 @@ METRICS = [
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
 ]
 PHASE = {"seg_reduce_kernel<1>": "fwd_segreduce", "seg_reduce_kernel<0>": "bwd_segreduce_adagrad",
-         "seg_fixup_kernel<1>": "fwd_fixup", "seg_fixup_kernel<0>": "bwd_fixup", "bag_expand_kernel": "bag_expand"}
+         "seg_fixup_lane_kernel<1>": "fwd_fixup", "seg_fixup_lane_kernel<0>": "bwd_fixup",
+         "bag_expand_kernel": "bag_expand"}
 
 
 def main():
