@@ -62,6 +62,22 @@ def build_workload(P, name):
     raise SystemExit(f"unknown workload {name}")
 
 
+def bench_plan(P, task, wname, world):
+    """The sharding plan of an N>1 run: the AutoShard-RL plan produced by the
+    reference trainer for this config and shard count (plans/<cfg>_k<N>_autoshard_rl.assignment,
+    oracle/rl_plans.cpp; BASELINE cfg 4 names the AutoShard-RL plan), else
+    lookup-greedy (planners.hpp:73-107)."""
+    for name in (f"{wname}_k{world}_autoshard_rl.assignment", f"{wname}_autoshard_rl.assignment"):
+        path = os.path.join(ROOT, "plans", name)
+        if os.path.exists(path):
+            a = [int(x) for x in open(path).read().split()]
+            if len(a) == len(task.tables) and max(a) < world:
+                plan = P.ShardingPlan(a)
+                if plan.feasible(task):
+                    return plan, f"autoshard-rl (plans/{name}, reference trainer)"
+    return P.greedy_shard(task, P.HeuristicKind.kLookupGreedy), "lookup-greedy (planners.hpp:73-107)"
+
+
 def nominal_bytes(tables, B, L, U):
     """SURVEY.md §8d algorithmic bytes (s = 4): per-phase split that sums to FWD+BWD."""
     s = 4
@@ -286,8 +302,7 @@ def main():
             raise SystemExit("batch must divide by the GPU count")
         budget = [int(180e9)] * world
         task = P.ShardingTask(tables_all, world, budget)
-        plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
-        plan_name = "lookup-greedy (planners.hpp:73-107)"
+        plan, plan_name = bench_plan(P, task, wname, world)
         mine = [t for t, k in zip(tables_all, plan.assignment) if k == rank]
     else:
         plan_name = "single shard"
@@ -367,6 +382,14 @@ def main():
     torch.cuda.synchronize()
     phase_ms, _ = shard.profile_read(reset=True)
     shard.profile(False)
+    # shard time = this rank's own kernels (serialized phases, no exchange): the
+    # paper's per-device cost C_k; max over ranks = max-shard time
+    ts = torch.tensor([sum(phase_ms.values()) / K], device="cuda", dtype=torch.float64)
+    shard_ms = [float(ts.item())]
+    if world > 1:
+        allt = [torch.zeros_like(ts) for _ in range(world)]
+        dist.all_gather(allt, ts)
+        shard_ms = [float(x.item()) for x in allt]
     fwd_b, bwd_b, phase_bytes = nominal_bytes(mine, B, L, U)
     peak, peak_kind = measured_peak_hbm()
     dom = max(phase_ms, key=phase_ms.get)
@@ -455,6 +478,9 @@ def main():
             "step_roofline": {"bytes_fwd": fwd_b, "bytes_bwd": bwd_b, "achieved_gbs": round(step_gbs, 1),
                               "frac": round(step_gbs / peak, 4)},
             "phase_ms_per_step": {k: round(v / K, 4) for k, v in phase_ms.items()},
+            "shard_ms_per_step": [round(x, 4) for x in shard_ms],
+            "max_shard_ms": round(max(shard_ms), 4),
+            "balance": round(min(shard_ms) / max(shard_ms), 4) if max(shard_ms) > 0 else 1.0,
             "gpu_launches": int(launches),
             "launches_per_step": launches / K,
             "e2e": e2e,

@@ -11,8 +11,23 @@
 // usage: rl_plans <n_pool> <n_target> <K> <batch> <max_updates> <max_seconds> <out_prefix> [dims...]
 // writes <out_prefix>.assignment (one line, n_target shard ids) and
 // <out_prefix>.ckpt (the reference checkpoint, ASHCKPT1).
+//
+// MARGINALS=<file>: train against B200-MEASURED costs
+// instead of the analytic SIM (tools/measure_marginals.py writes the file:
+// c0, rho and per-table marginals w_t = measured one-table time - c0). Every
+// task context gets marginal_w[t] = w_t (the env's terminal reward and the
+// cost-model bootstrap, rl.hpp:161-167 / rl_train.hpp:387-389), and the SIM
+// the trainer still evaluates directly (checkpoint selection through
+// measure_plan, rl_train.hpp:231) is CALIBRATED to the same measurements: c0
+// and rho from the file, a / b / cache_floor of SIM-1 (simcost.hpp:60-78)
+// least-squares fitted to the w_t on this workload.
 #include <chrono>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <sstream>
+#include <unordered_set>
 #include <fstream>
 #include <iostream>
 #include <memory>
@@ -46,7 +61,78 @@ int main(int argc, char** argv) {
   const std::vector<TableDesc> train_pool(pool.begin() + n_target, pool.end());
   const NormStats norm = compute_norm_stats(train_pool, wl);
   const FeatureMask mask{};
-  const SimParams sim{};
+  SimParams sim{};
+  std::map<int, double> measured;  // table id -> GPU marginal (ms)
+  if (const char* mf = std::getenv("MARGINALS")) {
+    std::ifstream is(mf);
+    if (!is) {
+      std::fprintf(stderr, "cannot read MARGINALS=%s\n", mf);
+      return 2;
+    }
+    std::string line;
+    while (std::getline(is, line)) {
+      if (line.empty() || line[0] == '#') continue;
+      std::istringstream ls(line);
+      std::string k;
+      double v;
+      ls >> k >> v;
+      if (k == "c0") sim.c0 = v;
+      else if (k == "rho") sim.rho = v;
+      else measured[std::atoi(k.c_str())] = v;
+    }
+    // fit SIM-1's a, b, cache_floor to the measured marginals of the pool
+    double best = 1e300, ba = sim.a, bb = sim.b, bf = sim.cache_floor;
+    std::vector<double> x1, x2, y;
+    std::vector<double> L, u, dim, lh;
+    for (const auto& t : pool) {
+      auto it = measured.find(t.id);
+      if (it == measured.end()) continue;
+      const TableStream* s = wl.find(t.id);
+      std::unordered_set<std::int64_t> d(s->indices.begin(), s->indices.end());
+      L.push_back((double)s->indices.size());
+      u.push_back(s->indices.empty() ? 0.0 : std::min(1.0, (double)d.size() / (double)s->indices.size()));
+      dim.push_back(t.dim);
+      lh.push_back(std::log10(1.0 + (double)t.hash_size));
+      y.push_back(it->second);
+    }
+    for (int g = 1; g <= 100; ++g) {
+      const double f = g / 100.0;
+      double s11 = 0, s12 = 0, s22 = 0, r1 = 0, r2 = 0;
+      std::vector<double> a1(y.size()), a2(y.size());
+      for (size_t i = 0; i < y.size(); ++i) {
+        a1[i] = L[i] * dim[i] * (f + (1 - f) * u[i]);
+        a2[i] = dim[i] * lh[i];
+        // relative least squares: weight 1/y^2
+        const double wgt = 1.0 / std::max(1e-9, y[i] * y[i]);
+        s11 += wgt * a1[i] * a1[i]; s12 += wgt * a1[i] * a2[i]; s22 += wgt * a2[i] * a2[i];
+        r1 += wgt * a1[i] * y[i]; r2 += wgt * a2[i] * y[i];
+      }
+      const double det = s11 * s22 - s12 * s12;
+      double a = det != 0 ? (r1 * s22 - r2 * s12) / det : 0, b = det != 0 ? (s11 * r2 - s12 * r1) / det : 0;
+      if (a < 0) { a = 0; b = r2 / s22; }
+      if (b < 0) { b = 0; a = r1 / s11; }
+      double err = 0;
+      for (size_t i = 0; i < y.size(); ++i) {
+        const double e = (a * a1[i] + b * a2[i] - y[i]) / std::max(1e-9, y[i]);
+        err += e * e;
+      }
+      if (err < best) { best = err; ba = a; bb = b; bf = f; }
+    }
+    sim.a = ba;
+    sim.b = bb;
+    sim.cache_floor = bf;
+    std::fprintf(stderr, "MARGINALS %s: %zu tables, c0 %.5f rho %.4f; SIM-1 fit a %.4g b %.4g cache_floor %.2f rel.RMS %.4f\n",
+                 mf, measured.size(), sim.c0, sim.rho, sim.a, sim.b, sim.cache_floor,
+                 std::sqrt(best / std::max<size_t>(1, y.size())));
+  }
+  auto with_measured = [&](rl::TaskContext ctx) {
+    if (!measured.empty())
+      for (size_t i = 0; i < ctx.task.tables.size(); ++i) {
+        auto it = measured.find(ctx.task.tables[i].id);
+        if (it != measured.end()) ctx.marginal_w[i] = it->second;
+      }
+    return ctx;
+  };
 
   auto task_of = [&](std::vector<TableDesc> tabs) {
     ShardingTask t;
@@ -64,9 +150,9 @@ int main(int argc, char** argv) {
     std::vector<TableDesc> tabs(train_pool);
     rng.shuffle(tabs.begin(), tabs.end());
     tabs.resize(std::min<size_t>(tabs.size(), (size_t)n_target));
-    train_tasks.push_back(rl::make_task_context(i, task_of(tabs), wl, norm, mask, sim));
+    train_tasks.push_back(with_measured(rl::make_task_context(i, task_of(tabs), wl, norm, mask, sim)));
   }
-  test_tasks.push_back(rl::make_task_context(1000, task_of(target), wl, norm, mask, sim));
+  test_tasks.push_back(with_measured(rl::make_task_context(1000, task_of(target), wl, norm, mask, sim)));
 
   rl::TrainConfig cfg;
   cfg.max_updates = max_updates;
