@@ -320,18 +320,34 @@ def main():
 
     # N>1: table-wise shards; pooled rows go to their sample owners and the
     # gradient comes back with the inverse all-to-all (paper_2208_06399_b200.sharded)
+    exchange = None
     if world > 1:
-        from paper_2208_06399_b200.sharded import PooledExchange, a2a_layout
+        from paper_2208_06399_b200.sharded import FusedPooledExchange, PooledExchange, a2a_layout
 
-        exch = PooledExchange(a2a_layout(task, plan, B), rank, device="cuda")
+        lay = a2a_layout(task, plan, B)
+        exch = None
+        if os.environ.get("ASB_FUSED_A2A", "1") != "0":
+            try:  # forward exchange fused into the forward kernel (peer stores, symmetric memory)
+                exch = FusedPooledExchange(lay, rank, shard, device="cuda")
+                exchange = "fused: pooled rows stored into the sample owners' symmetric-memory receive buffers by the " \
+                           "forward kernel + device barrier; backward: NCCL all_to_all_single"
+            except Exception as e:  # noqa: BLE001
+                exchange = f"NCCL all_to_all_single both ways (symmetric memory unavailable: {type(e).__name__})"
+        if exch is None:
+            exch = PooledExchange(lay, rank, device="cuda")
+            exchange = exchange or "NCCL all_to_all_single both ways"
 
     def step():
-        shard.forward(pooled, stream=stream)
         if world > 1:
-            recv = exch.forward(pooled)
+            if isinstance(exch, FusedPooledExchange):
+                recv = exch.forward(stream=stream)
+            else:
+                shard.forward(pooled, stream=stream)
+                recv = exch.forward(pooled)
             # dense part out of scope: loss 1/2|pooled|^2 -> dL/dpooled = pooled (recv)
             shard.backward(exch.backward(recv), LR, EPS, stream=stream)
         else:
+            shard.forward(pooled, stream=stream)
             shard.backward(pooled, LR, EPS, stream=stream)
 
     props = torch.cuda.get_device_properties(local)
@@ -468,8 +484,9 @@ def main():
                 "lookups": int(sum(L)) if world == 1 else None,
                 "plan": plan_name,
                 "parallelism": "table-wise" if world > 1 else "single",
+                "exchange": exchange,
                 "step": "K4 bag-expand + fwd segreduce + fixup + radix sort + bwd segreduce/row-wise Adagrad + fixup"
-                        + (" + 2x NCCL all_to_all" if world > 1 else "") + "; grad = pooled (loss 1/2|pooled|^2)",
+                        + (" + pooled-row exchange both ways" if world > 1 else "") + "; grad = pooled (loss 1/2|pooled|^2)",
                 "l2": "flushed (2x L2 fill) between timed steps, flush excluded from step time",
                 "lr": LR,
                 "eps": EPS,

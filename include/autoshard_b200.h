@@ -203,6 +203,19 @@ AS_API as_status as_check_batch(as_ctx* ctx);
  * out: device [batch, sum_dim] fp32, or NULL for the ctx's own buffer. */
 AS_API as_status as_forward(as_ctx* ctx, float* out_or_null, void* stream);
 
+/* Fused forward exchange for table-wise sharding over G GPUs (
+ * replaces the pooled-row all-to-all that follows the forward). Once set,
+ * as_forward writes pooled row b of every table of this shard to the receive
+ * buffer of the sample owner q = b / rows_per_peer, at
+ *   peer_bases[q] + (b - q * rows_per_peer) * sum_dim + col_t
+ * (peer_bases[q]: a device address valid on this ctx's device — the owner's
+ * receive block for this shard, e.g. from torch symmetric memory / CUDA IPC;
+ * on another GPU the epilogue's stores go over NVLink), and ignores
+ * out_or_null. The caller orders readers after the writers (a barrier after
+ * the forward). n_peers = 0 restores the local [batch, sum_dim] output.
+ * AS_SHAPE unless n_peers * rows_per_peer == batch; at most 8 peers. */
+AS_API as_status as_set_peer_outputs(as_ctx* ctx, int n_peers, float* const* peer_bases, int64_t rows_per_peer);
+
 /* K2+K3: sort (row, bag), segment-sum the gradient rows per unique row and
  * apply exact row-wise Adagrad in place:
  *   m_r += |g_r|^2 / dim ;  W_r -= lr * g_r / (sqrt(m_r) + eps).

@@ -111,6 +111,7 @@ SIGNATURES = {
     "as_commit_staged": (i32, [vp, vp]),
     "as_check_batch": (i32, [vp]),
     "as_forward": (i32, [vp, vp, vp]),
+    "as_set_peer_outputs": (i32, [vp, i32, P(vp), i64]),
     "as_backward_rowwise_adagrad": (i32, [vp, vp, f32, f32, vp]),
     "as_step": (i32, [vp, f32, f32, P(f64), vp]),
     "as_measure": (i32, [vp, i32, i32, i32, i32, f32, f32, P(f64)]),

@@ -400,6 +400,14 @@ AS_API as_status as_forward(as_ctx* ctx, float* out, void* stream) {
   });
 }
 
+AS_API as_status as_set_peer_outputs(as_ctx* ctx, int n_peers, float* const* peer_bases, int64_t rows_per_peer) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (n_peers > 0) need(peer_bases, "peer_bases");
+    ctx->impl->set_peer_outputs(n_peers, peer_bases, rows_per_peer);
+  });
+}
+
 AS_API as_status as_backward_rowwise_adagrad(as_ctx* ctx, const float* grad, float lr, float eps, void* stream) {
   return guard([&] {
     need(ctx, "ctx");

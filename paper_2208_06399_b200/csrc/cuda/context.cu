@@ -746,7 +746,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   {
     Phase ph(this, 0, s);
     bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
-                                                                            target, sum_dim_);
+                                                                            target, sum_dim_, peers_);
     cuda_check(cudaGetLastError(), "bag_expand_kernel");
     ++launches_;
   }
@@ -762,6 +762,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   p.W_ro = W_;
   p.out = target;
   p.out_stride = sum_dim_;
+  p.peers = peers_;
   p.loss = loss_dev;
   cuda_check(cudaMemsetAsync(counters_, 0, sizeof(int) * 3, s), "counter reset");
   {
@@ -817,6 +818,9 @@ void EmbContext::launch_sort(cudaStream_t s) {
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
   require_loaded("as_backward_rowwise_adagrad");
+  if (!grad && peers_.n)
+    fail(AS_STATE, "as_backward_rowwise_adagrad: the forward writes to peer buffers (as_set_peer_outputs); pass the "
+                   "gradient of this shard's pooled rows");
   DeviceGuard g(device_);
   if (T_ == 0 || n_chunks_ == 0) return;
   if (sort_pending_) {
@@ -847,8 +851,28 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   launches_ += 3;
 }
 
+void EmbContext::set_peer_outputs(int n, float* const* bases, int64_t rows) {
+  if (n == 0) {
+    std::memset(&peers_, 0, sizeof peers_);
+    return;
+  }
+  if (n < 0 || n > kMaxPeers) fail(AS_CONFIG, "as_set_peer_outputs: 0..8 peers, got " + std::to_string(n));
+  if (rows < 1 || rows * n != B_)
+    fail(AS_SHAPE, "as_set_peer_outputs: " + std::to_string(n) + " peers x " + std::to_string(rows) +
+                       " rows must cover the batch of " + std::to_string(B_));
+  for (int q = 0; q < n; ++q)
+    if (!bases[q]) fail(AS_CONFIG, "as_set_peer_outputs: peer " + std::to_string(q) + " has a NULL base");
+  std::memset(&peers_, 0, sizeof peers_);
+  for (int q = 0; q < n; ++q) peers_.base[q] = bases[q];
+  peers_.n = n;
+  peers_.rows = static_cast<int>(rows);
+}
+
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {
   require_loaded("as_step");
+  if (peers_.n)
+    fail(AS_STATE, "as_step: the forward writes to peer buffers (as_set_peer_outputs); run as_forward, the "
+                   "exchange and as_backward_rowwise_adagrad");
   DeviceGuard g(device_);
   if (loss_host) cuda_check(cudaMemsetAsync(loss_, 0, sizeof(double), s), "loss reset");
   forward(out_, loss_host ? loss_ : nullptr, s);

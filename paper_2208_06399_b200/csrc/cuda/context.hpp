@@ -32,6 +32,7 @@ class EmbContext {
   void check();
   void forward(float* out, double* loss_dev, cudaStream_t s);
   void backward(const float* grad, float lr, float eps, cudaStream_t s);
+  void set_peer_outputs(int n, float* const* bases, int64_t rows);
   void step(float lr, float eps, double* loss_host, cudaStream_t s);
   double measure(int warmup, int measure, int trim, bool flush, float lr, float eps);
 
@@ -141,6 +142,7 @@ class EmbContext {
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
   int64_t n_tma_units_ = 0;
+  PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
   double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
   double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)

@@ -125,13 +125,21 @@ __device__ __forceinline__ float group_sum(float x, unsigned mask) {
   return x;
 }
 
+// Row `b` of the pooled output: local [B, stride] buffer, or the receive
+// buffer of the sample's owner (fused exchange, PeerOut).
+__device__ __forceinline__ float* pooled_row(float* out, long long stride, const PeerOut& peers, int b) {
+  if (peers.n == 0) return out + (long long)b * stride;
+  const int q = b / peers.rows;
+  return peers.base[q] + (long long)(b - q * peers.rows) * stride;
+}
+
 // Segment epilogues, executed by the GL lanes of one group.
 // forward : pooled[bag, col_t + :] = v   (+ loss 1/2|v|^2)
 template <int GL, int NV>
 __device__ __forceinline__ void store_pooled(const SegParams& p, const DevTable& tb, int seg, const float4 (&v)[NV],
                                              int c, float& loss_acc) {
   const int nvec = tb.dim >> 2;
-  float* o = p.out + (long long)seg * p.out_stride + tb.col;
+  float* o = pooled_row(p.out, p.out_stride, p.peers, seg) + tb.col;
 #pragma unroll
   for (int w = 0; w < NV; ++w) {
     const int cv = c + w * GL;
@@ -781,7 +789,7 @@ __global__ void __launch_bounds__(256) seg_fixup_long_kernel(SegParams p) {
 __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__ off, int T, int B,
                                                          const DevTable* __restrict__ tabs,
                                                          int* __restrict__ bag, float* __restrict__ out,
-                                                         long long out_stride) {
+                                                         long long out_stride, PeerOut peers) {
   const long long nb = (long long)T * B;
   const long long w0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
   if (w0 >= nb) return;
@@ -812,7 +820,7 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
     const int ti = __shfl_sync(0xffffffffu, t, i);
     const int bi = __shfl_sync(0xffffffffu, b, i);
     const int nvec = tabs[ti].dim >> 2;
-    float* row = out + (long long)bi * out_stride + tabs[ti].col;
+    float* row = pooled_row(out, out_stride, peers, bi) + tabs[ti].col;
     for (int cv = lane; cv < nvec; cv += 32) st4_streaming(row + cv * 4, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }

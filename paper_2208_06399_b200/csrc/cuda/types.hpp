@@ -49,6 +49,18 @@ __host__ __device__ constexpr int kind_gl(int k) {
 __host__ __device__ constexpr int kind_nv(int k) { return k <= 5 ? 1 : (k <= 8 ? 1 << (k - 5) : (k <= 10 ? 2 : 4)); }
 constexpr int kNumKinds = 13;
 
+// Fused forward exchange (table-wise sharding): pooled row b
+// goes straight to the receive buffer of its sample owner q = b / rows, at
+// base[q] + (b - q*rows) * out_stride + col_t — on another GPU a peer
+// (NVLink) store, so the all-to-all of the pooled rows rides on the K1
+// epilogue. n = 0: the plain [B, sum_dim] output.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  float* base[kMaxPeers];
+  int n;
+  int rows;
+};
+
 struct SegParams {
   const DevTable* tabs;
   const int* unit_table;  // warp unit -> table position
@@ -61,6 +73,7 @@ struct SegParams {
   float* out;
   long long out_stride;
   double* loss;  // optional: += 1/2 sum of squares of the pooled rows
+  PeerOut peers;
   // backward
   const float* grad;
   long long grad_stride;

@@ -131,6 +131,14 @@ class EmbeddingShard:
     def forward(self, out=None, stream=None) -> None:
         check(lib().as_forward(self._h, _ptr(out), _stream(stream)))
 
+    def set_peer_outputs(self, bases, rows_per_peer: int) -> None:
+        """Fused forward exchange (as_set_peer_outputs): pooled row b goes to
+        bases[b // rows_per_peer] (device addresses, e.g. symmetric-memory peer
+        buffers); bases=[] restores the local output."""
+        n = len(bases)
+        arr = (C.c_void_p * max(1, n))(*[int(b) for b in bases])
+        check(lib().as_set_peer_outputs(self._h, n, arr, int(rows_per_peer) if n else 0))
+
     def backward(self, grad=None, lr: float = 0.01, eps: float = 1e-8, stream=None) -> None:
         check(lib().as_backward_rowwise_adagrad(self._h, _ptr(grad), lr, eps, _stream(stream)))
 

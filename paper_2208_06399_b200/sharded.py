@@ -11,7 +11,9 @@ rank p receives G blocks [B/G, SD_k] in rank order. The backward exchange is
 the exact inverse for the gradient of those rows.
 
 The collectives go through ``torch.distributed`` (NCCL over NVLink on the
-GPU box, gloo in the CPU tests); this module holds only the layout logic.
+GPU box, gloo in the CPU tests). ``FusedPooledExchange`` removes the forward
+collective: the forward kernel itself stores each pooled row into its sample
+owner's receive buffer (torch symmetric memory, peer stores over NVLink).
 """
 from __future__ import annotations
 
@@ -116,3 +118,52 @@ class PooledExchange:
         k = members.index(table_pos)
         cols = self.L.columns[owner] + [self.L.shard_dims[owner]]
         return cols[k + 1] - cols[k]
+
+
+def peer_bases(layout: A2ALayout, owner: int, recv_base_ptrs: Sequence[int]) -> List[int]:
+    """Device addresses the owner's forward writes to (as_set_peer_outputs):
+    for every sample owner q, q's receive buffer + this owner's block offset."""
+    return [int(p) + 4 * layout.recv_offset(owner) for p in recv_base_ptrs]
+
+
+class FusedPooledExchange:
+    """Forward exchange fused into the forward kernel: the
+    receive buffers live in torch symmetric memory (one allocation per rank,
+    mapped into every peer over NVLink), the shard's K1/K4 epilogues store each
+    pooled row straight into its sample owner's receive block
+    (EmbeddingShard.set_peer_outputs), and a device-side barrier orders the
+    readers. No pooled-row copy, no NCCL call in the forward. The backward
+    exchange of the gradients stays the NCCL all-to-all (PooledExchange).
+
+    Raises when symmetric memory is unavailable; callers fall back to
+    PooledExchange."""
+
+    def __init__(self, layout: A2ALayout, rank: int, shard, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.L, self.rank, self.group = layout, rank, group
+        group = group or dist.group.WORLD
+        try:
+            symm_mem.enable_symm_mem_for_group(group.group_name)
+        except Exception:
+            pass
+        n = layout.rows_per_rank * sum(layout.shard_dims)
+        self.recv_buf = symm_mem.empty(n, dtype=torch.float32, device=device)
+        self.hdl = symm_mem.rendezvous(self.recv_buf, group)
+        self.shard = shard
+        shard.set_peer_outputs(peer_bases(layout, rank, self.hdl.buffer_ptrs), layout.rows_per_rank)
+        self._nccl = PooledExchange(layout, rank, group=self.group, device=device)
+
+    def forward(self, stream=None):
+        """This rank's forward with the exchange fused in; returns the receive buffer."""
+        self.shard.forward(stream=stream)
+        self.hdl.barrier(channel=0)  # every owner's stores into every receive buffer are done
+        return self.recv_buf
+
+    def backward(self, grad_recv):
+        return self._nccl.backward(grad_recv)
+
+    def close(self):
+        self.shard.set_peer_outputs([], 0)

@@ -100,3 +100,18 @@ def test_layout_splits_and_locate(P):
         assert plan.assignment[i] == k
     with pytest.raises(ValueError):
         a2a_layout(task, plan, 4095)
+
+
+def test_peer_bases_match_receive_layout():
+    """as_set_peer_outputs addresses (fused exchange) = receive buffer + the owner's block offset."""
+    import paper_2208_06399_b200 as P
+    from paper_2208_06399_b200.sharded import a2a_layout, peer_bases
+
+    pool = P.generate_pool(0, 9, P.GeneratorConfig(dim_choices=(16, 32, 64)))
+    task = P.ShardingTask(pool, 3, [1 << 40] * 3)
+    plan = P.random_shard(task, 2)
+    lay = a2a_layout(task, plan, 96)
+    bases = [1 << 20, 2 << 20, 3 << 20]
+    for k in range(3):
+        got = peer_bases(lay, k, bases)
+        assert got == [b + 4 * 32 * sum(lay.shard_dims[:k]) for b in bases]
