@@ -512,6 +512,39 @@ def main():
         dist.destroy_process_group()
 
 
+def reference_pieces(P, tables, B, wl):
+    """the reference's own CPU pieces on the path, timed single-threaded
+    as the reference runs them (oracle/_ref/libref.so = the unmodified headers compiled
+    in place), next to this repo's host equivalents on the same inputs."""
+    try:
+        from oracle import Ref, Table
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    try:
+        ref = Ref()
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)}
+    otabs = [Table(t.id, t.dim, t.hash_size, t.pooling_mean, t.access_ratio, t.bytes_per_param) for t in tables]
+    budgets = [sum(t.size_bytes() for t in tables)]
+    out = {"threads": 1, "tables": len(tables), "batch": B}
+    t0 = time.perf_counter()
+    h, _ = ref.generate_workload(0, otabs, B)
+    out["generate_workload_s"] = round(time.perf_counter() - t0, 3)
+    t0 = time.perf_counter()
+    ref.measure_plan(otabs, budgets, [0] * len(otabs), h)
+    out["measure_plan_sim_s"] = round(time.perf_counter() - t0, 3)
+    t0 = time.perf_counter()
+    for k in (0, 1, 2):
+        ref.greedy_shard(otabs, budgets, k)
+    out["greedy_x3_s"] = round(time.perf_counter() - t0, 6)
+    ref.free_workload(h)
+    t0 = time.perf_counter()
+    P.generate_workload(0, tables, B)
+    out["ours_generate_workload_s"] = round(time.perf_counter() - t0, 3)
+    out["ours_generate_workload_threads"] = os.cpu_count()
+    return out
+
+
 def run_reference(args, world, rank, wname):
     """CPU arm: the reference has no embedding arithmetic, so the
     reference-side implementation of the path is the oracle port (fp32, OpenMP,
@@ -522,6 +555,7 @@ def run_reference(args, world, rank, wname):
 
     tables, B, wdesc = build_workload(P, wname)
     wl = P.generate_workload(0, tables, B)
+    pieces = reference_pieces(P, tables, B, wl) if os.environ.get("ASB_REF_PIECES", "1") != "0" else None
     cs = CpuSample(tables, wl, B)
     for _ in range(args.warmup):
         cs.step()
@@ -544,6 +578,7 @@ def run_reference(args, world, rank, wname):
         "data": "synthetic (reference generator, bit-exact)",
         "config": {"workload": wname, "desc": wdesc, "tables": len(tables), "global_batch": B},
         "cpu_baseline": cpu,
+        "reference_pieces": pieces,
         "e2e": {"value": round(v, 2), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
