@@ -78,8 +78,9 @@ def bench_plan(P, task, wname, world):
     return P.greedy_shard(task, P.HeuristicKind.kLookupGreedy), "lookup-greedy (planners.hpp:73-107)"
 
 
-def nominal_bytes(tables, B, L, U):
-    """SURVEY.md §8d algorithmic bytes (s = 4): per-phase split that sums to FWD+BWD."""
+def nominal_bytes(tables, B, L, U, wb=4):
+    """SURVEY.md §8d algorithmic bytes (s = 4; weights wb = 4, or 2 for fp16
+    storage): per-phase split that sums to FWD+BWD."""
     s = 4
     T = len(tables)
     SD = sum(t.dim for t in tables)
@@ -88,14 +89,14 @@ def nominal_bytes(tables, B, L, U):
     Lt, Ut = sum(L), sum(U)
     phases = {
         "bag_expand": s * T * (B + 1),
-        "fwd_segreduce": s * (Lt + LD + B * SD),
+        "fwd_segreduce": s * (Lt + B * SD) + wb * LD,
         "fwd_fixup": 0,
         "radix_sort": s * (Lt + T * (B + 1)),
-        "bwd_segreduce_adagrad": s * LD + 2 * s * UD + 2 * s * Ut,
+        "bwd_segreduce_adagrad": s * LD + 2 * wb * UD + 2 * s * Ut,
         "bwd_fixup": 0,
     }
-    fwd = s * (Lt + T * (B + 1) + LD + B * SD)
-    bwd = s * (Lt + T * (B + 1) + LD) + 2 * s * UD + 2 * s * Ut
+    fwd = s * (Lt + T * (B + 1) + B * SD) + wb * LD
+    bwd = s * (Lt + T * (B + 1) + LD) + 2 * wb * UD + 2 * s * Ut
     return fwd, bwd, phases
 
 
@@ -272,6 +273,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="auto",
                     help="cfg1|cfg2|cfg2u|cfg3|cfg4 (auto: cfg2 at N=1, cfg4 at N>1)")
+    ap.add_argument("--weights", choices=["fp32", "fp16"], default="fp32",
+                    help="table storage (fp16 = bytes_per_param 2, as_create_ex AS_WEIGHTS_FP16; fp32 accumulation)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
@@ -312,7 +315,7 @@ def main():
     wl = P.generate_workload(0, mine, B, zipf)  # subset-stable: identical to the full-pool streams
     wl.pin()
     L, U = stream_stats(wl, mine)
-    shard = P.EmbeddingShard(mine, B, device=local, weight_seed=WEIGHT_SEED)
+    shard = P.EmbeddingShard(mine, B, device=local, weight_seed=WEIGHT_SEED, weights=args.weights)
     shard.load(wl)
     stream = torch.cuda.current_stream()
     SD = shard.sum_dim
@@ -406,12 +409,12 @@ def main():
         allt = [torch.zeros_like(ts) for _ in range(world)]
         dist.all_gather(allt, ts)
         shard_ms = [float(x.item()) for x in allt]
-    fwd_b, bwd_b, phase_bytes = nominal_bytes(mine, B, L, U)
+    fwd_b, bwd_b, phase_bytes = nominal_bytes(mine, B, L, U, wb=2 if args.weights == "fp16" else 4)
     peak, peak_kind = measured_peak_hbm()
     dom = max(phase_ms, key=phase_ms.get)
     dom_ms = phase_ms[dom] / K
     achieved = phase_bytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    traffic = ncu_traffic(dom, wname) if world == 1 else None
+    traffic = ncu_traffic(dom, wname) if world == 1 and args.weights == "fp32" else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "algorithmic_bytes_per_launch": phase_bytes[dom],
@@ -473,7 +476,7 @@ def main():
             "higher_is_better": True,
             "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": None,
-            "dtype": "fp32",
+            "dtype": "fp32" if args.weights == "fp32" else "fp32 (fp16 table storage)",
             "data": "synthetic (reference generator, bit-exact; weights: counter-hash grid init)",
             "config": {
                 "workload": wname,
@@ -483,6 +486,7 @@ def main():
                 "sum_dim": sum(t.dim for t in tables_all),
                 "lookups": int(sum(L)) if world == 1 else None,
                 "plan": plan_name,
+                "weights": args.weights,
                 "parallelism": "table-wise" if world > 1 else "single",
                 "exchange": exchange,
                 "step": "K4 bag-expand + fwd segreduce + fixup + radix sort + bwd segreduce/row-wise Adagrad + fixup"

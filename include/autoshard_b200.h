@@ -167,6 +167,15 @@ AS_API as_status as_plan_load(const char* path, const as_table_spec* tables, int
  * columns are laid out in that order. n_tables may be 0 (empty shard). */
 AS_API as_status as_create(int32_t device, const as_table_spec* tables, int32_t n_tables,
                            int64_t batch_size, uint64_t weight_seed, as_ctx** out);
+
+/* as_create with flags. AS_WEIGHTS_FP16: tables stored as IEEE fp16
+ * (bytes_per_param = 2, tables.hpp:30) — the
+ * forward gathers half rows and accumulates in fp32, the row-wise Adagrad
+ * update is computed in fp32 and rounded to nearest fp16; momentum, pooled
+ * rows and gradients stay fp32. Unknown flags: AS_CONFIG. */
+#define AS_WEIGHTS_FP16 1
+AS_API as_status as_create_ex(int32_t device, const as_table_spec* tables, int32_t n_tables,
+                              int64_t batch_size, uint64_t weight_seed, int32_t flags, as_ctx** out);
 AS_API as_status as_destroy(as_ctx* ctx);
 
 /* Load one batch of streams (host int64 CSR per table, ctx table order,
@@ -255,10 +264,10 @@ typedef struct as_ctx_info {
   int64_t n_chunks;      /* work chunks of the loaded batch */
   int64_t device_bytes;  /* bytes allocated on the device */
   float* pooled;         /* device [batch, sum_dim] */
-  float* weights;        /* device, concatenated [hash_t, dim_t] */
+  float* weights;        /* device, concatenated [hash_t, dim_t] (fp16 if weight_bytes == 2) */
   float* momentum;       /* device [total_rows] */
   int32_t kernels_per_step; /* kernel launches of one as_step */
-  int32_t _pad;
+  int32_t weight_bytes;     /* 4 (fp32) or 2 (AS_WEIGHTS_FP16) */
 } as_ctx_info;
 AS_API as_status as_ctx_info_get(const as_ctx* ctx, as_ctx_info* info);
 

@@ -66,7 +66,7 @@ class CtxInfoC(C.Structure):
         ("weights", C.c_void_p),
         ("momentum", C.c_void_p),
         ("kernels_per_step", C.c_int32),
-        ("_pad", C.c_int32),
+        ("weight_bytes", C.c_int32),
     ]
 
 
@@ -103,6 +103,7 @@ SIGNATURES = {
     "as_plan_save": (i32, [C.c_char_p, T_SPEC, i32, i32, P(i64), P(i32), P(f64)]),
     "as_plan_load": (i32, [C.c_char_p, T_SPEC, i32, i32, P(i64), P(i32), P(f64), P(i32)]),
     "as_create": (i32, [i32, T_SPEC, i32, i64, u64, P(vp)]),
+    "as_create_ex": (i32, [i32, T_SPEC, i32, i64, u64, i32, P(vp)]),
     "as_destroy": (i32, [vp]),
     "as_load_streams": (i32, [vp, P(vp), P(vp), P(i64), vp]),
     "as_load_workload": (i32, [vp, vp, vp]),

@@ -321,15 +321,20 @@ AS_API as_status as_plan_load(const char* path, const as_table_spec* t, int32_t 
 }
 
 // ---- device context -----------------------------------------------------
-AS_API as_status as_create(int32_t device, const as_table_spec* tables, int32_t n, int64_t batch, uint64_t seed,
-                           as_ctx** out) {
+AS_API as_status as_create_ex(int32_t device, const as_table_spec* tables, int32_t n, int64_t batch, uint64_t seed,
+                              int32_t flags, as_ctx** out) {
   return guard([&] {
     need(out, "out");
     if (n > 0) need(tables, "tables");
     auto c = std::make_unique<as_ctx>();
-    c->impl = std::make_unique<asb::EmbContext>(device, tables, n, batch, seed);
+    c->impl = std::make_unique<asb::EmbContext>(device, tables, n, batch, seed, flags);
     *out = c.release();
   });
+}
+
+AS_API as_status as_create(int32_t device, const as_table_spec* tables, int32_t n, int64_t batch, uint64_t seed,
+                           as_ctx** out) {
+  return as_create_ex(device, tables, n, batch, seed, 0, out);
 }
 
 AS_API as_status as_destroy(as_ctx* ctx) {

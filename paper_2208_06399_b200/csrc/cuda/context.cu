@@ -91,7 +91,7 @@ int bit_width_u64(uint64_t x) {
   return b;
 }
 
-__global__ void gather_rows_kernel(const float* __restrict__ src, long long w_off, int dim,
+__global__ void gather_rows_kernel(const void* __restrict__ src, int half, long long w_off, int dim,
                                    const long long* __restrict__ rows, long long n,
                                    float* __restrict__ dst) {
   const long long total = n * dim;
@@ -99,7 +99,8 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, long long w_of
        q += (long long)gridDim.x * blockDim.x) {
     const long long i = q / dim;
     const int d = (int)(q - i * dim);
-    dst[q] = src[w_off + rows[i] * dim + d];
+    const long long e = w_off + rows[i] * dim + d;
+    dst[q] = half ? __half2float(reinterpret_cast<const __half*>(src)[e]) : reinterpret_cast<const float*>(src)[e];
   }
 }
 
@@ -179,8 +180,9 @@ void* EmbContext::dalloc(size_t bytes) {
   return p;
 }
 
-EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed)
-    : device_(device), T_(n), B_(batch), seed_(seed) {
+EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed, int flags)
+    : device_(device), T_(n), B_(batch), seed_(seed), w_half_((flags & AS_WEIGHTS_FP16) != 0) {
+  if (flags & ~AS_WEIGHTS_FP16) fail(AS_CONFIG, "as_create_ex: unknown flags " + std::to_string(flags));
   if (n < 0) fail(AS_CONFIG, "as_create: n_tables must be >= 0");
   if (batch < 1 || batch > (1LL << 30)) fail(AS_CONFIG, "as_create: batch_size must be in [1, 2^30]");
   int ndev = 0;
@@ -230,7 +232,7 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
 
   DeviceGuard g(device_);
   dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
-  W_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_w_)));
+  W_ = static_cast<float*>(dalloc((w_half_ ? 2 : 4) * static_cast<size_t>(total_w_)));
   M_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_rows_)));
   out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
   for (Slot& sl : slots_) {
@@ -262,10 +264,13 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)) + 1);
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    pct),
+               "carveout");
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
   }
-  if (const char* e = std::getenv("ASB_TMA")) use_tma_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("ASB_TMA")) use_tma_ = std::atoi(e) != 0 && !w_half_;
   cuda_check(cudaFuncSetAttribute(seg_reduce_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kTmaSmemBytes),
              "tma smem");
@@ -283,7 +288,11 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   for (int t = 0; t < n; ++t) {
     const long long nv = specs_[t].hash_size * (specs_[t].dim / 4);
     const unsigned grid = static_cast<unsigned>(std::min<long long>((nv + 255) / 256, 148LL * 64));
-    init_table_kernel<<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
+    if (w_half_)
+      init_table_kernel<true><<<grid, 256>>>(reinterpret_cast<__half*>(W_) + off, specs_[t].hash_size, specs_[t].dim,
+                                             specs_[t].id, s0);
+    else
+      init_table_kernel<false><<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
     off += specs_[t].hash_size * specs_[t].dim;
   }
   cuda_check(cudaGetLastError(), "init_table_kernel");
@@ -715,6 +724,7 @@ SegParams EmbContext::seg_params(bool fwd) const {
   p.carry_stride = max_dim_;
   p.stage_x = stage_x_;
   p.stage_s = stage_s_;
+  p.w_half = w_half_ ? 1 : 0;
   return p;
 }
 
@@ -731,7 +741,11 @@ void EmbContext::launch_seg(SegParams p, cudaStream_t s) {
   }
   if (n_units_ > n_tma_units_) {
     p.unit_begin = (int)n_tma_units_;
-    seg_reduce_kernel<FWD><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
+    if (FWD && w_half_)
+      seg_reduce_kernel<true, true><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(
+          p);
+    else
+      seg_reduce_kernel<FWD><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
     cuda_check(cudaGetLastError(), "seg_reduce_kernel");
     ++launches_;
   }
@@ -980,7 +994,8 @@ void EmbContext::read_rows(int t, const int64_t* rows, int64_t n, float* out) {
   cuda_check(cudaMalloc(&dst, sizeof(float) * n * specs_[t].dim), "malloc");
   cuda_check(cudaMemcpy(drows, rows, sizeof(long long) * n, cudaMemcpyHostToDevice), "rows H2D");
   const long long w_off = htabs_[t].w_base;
-  gather_rows_kernel<<<grid_for(n * specs_[t].dim, 256), 256>>>(W_, w_off, specs_[t].dim, drows, n, dst);
+  gather_rows_kernel<<<grid_for(n * specs_[t].dim, 256), 256>>>(W_, w_half_ ? 1 : 0, w_off, specs_[t].dim, drows, n,
+                                                                 dst);
   cuda_check(cudaGetLastError(), "gather_rows_kernel");
   cuda_check(cudaMemcpy(out, dst, sizeof(float) * n * specs_[t].dim, cudaMemcpyDeviceToHost), "rows D2H");
   cudaFree(drows);
@@ -1033,7 +1048,15 @@ void EmbContext::write_table(int t, const float* w, const float* m) {
   const size_t rows = static_cast<size_t>(specs_[t].hash_size);
   if (w) {
     const long long w_off = htabs_[t].w_base;
-    cuda_check(cudaMemcpy(W_ + w_off, w, sizeof(float) * rows * specs_[t].dim, cudaMemcpyHostToDevice), "W H2D");
+    const size_t n = rows * specs_[t].dim;
+    if (w_half_) {
+      std::vector<__half> h(n);
+      for (size_t i = 0; i < n; ++i) h[i] = __float2half_rn(w[i]);
+      cuda_check(cudaMemcpy(reinterpret_cast<__half*>(W_) + w_off, h.data(), sizeof(__half) * n, cudaMemcpyHostToDevice),
+                 "W H2D");
+    } else {
+      cuda_check(cudaMemcpy(W_ + w_off, w, sizeof(float) * n, cudaMemcpyHostToDevice), "W H2D");
+    }
   }
   if (m) cuda_check(cudaMemcpy(M_ + htabs_[t].row_off, m, sizeof(float) * rows, cudaMemcpyHostToDevice), "M H2D");
 }
@@ -1052,6 +1075,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->weights = W_;
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
+  o->weight_bytes = w_half_ ? 2 : 4;
   o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 9 + 2 + sort_passes_);
 }
 

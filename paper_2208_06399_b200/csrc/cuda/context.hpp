@@ -18,7 +18,7 @@ void cuda_check(cudaError_t e, const char* what);
 
 class EmbContext {
  public:
-  EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed);
+  EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed, int flags = 0);
   ~EmbContext();
   EmbContext(const EmbContext&) = delete;
   EmbContext& operator=(const EmbContext&) = delete;
@@ -66,6 +66,7 @@ class EmbContext {
   int T_;
   int64_t B_;
   uint64_t seed_;
+  bool w_half_ = false;  // AS_WEIGHTS_FP16: W stored as __half
   std::vector<as_table_spec> specs_;
   std::vector<DevTable> htabs_;
   int64_t sum_dim_ = 0, total_rows_ = 0, total_w_ = 0;

@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "types.hpp"
@@ -82,6 +83,33 @@ __device__ __forceinline__ float4 shfl4_up(float4 v, int d) {
                      __shfl_up_sync(0xffffffffu, v.z, d), __shfl_up_sync(0xffffffffu, v.w, d));
 }
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+// fp16 weights: 4 halves (8 B) -> float4, and back with round-to-nearest
+__device__ __forceinline__ float4 half4_to_float4(uint2 r) {
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&r.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&r.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ uint2 float4_to_half4(float4 v) {
+  const __half2 a = __floats2half2_rn(v.x, v.y);
+  const __half2 b = __floats2half2_rn(v.z, v.w);
+  return make_uint2(*reinterpret_cast<const unsigned*>(&a), *reinterpret_cast<const unsigned*>(&b));
+}
+__device__ __forceinline__ float4 ldg_h4(const char* p) {
+  return half4_to_float4(__ldg(reinterpret_cast<const uint2*>(p)));
+}
+// Row slice of W (cv-th float4 of row `seg`) in either storage type.
+__device__ __forceinline__ float4 load_w4(const SegParams& p, const DevTable& tb, int seg, int cv) {
+  const long long e = tb.w_base + (long long)seg * tb.dim + cv * 4;
+  if (p.w_half) return half4_to_float4(*reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(p.W) + e));
+  return *reinterpret_cast<const float4*>(p.W + e);
+}
+__device__ __forceinline__ void store_w4(const SegParams& p, const DevTable& tb, int seg, int cv, float4 x) {
+  const long long e = tb.w_base + (long long)seg * tb.dim + cv * 4;
+  if (p.w_half)
+    *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.W) + e) = float4_to_half4(x);
+  else
+    *reinterpret_cast<float4*>(p.W + e) = x;
+}
 
 // L2 eviction priorities (ASB_L2HINTS): gathered rows (re-read ~L/U times)
 // evict_last, the streamed index arrays evict_first.
@@ -103,9 +131,19 @@ __device__ __forceinline__ float4 ldg4_hint(const float* p, unsigned long long p
   return v;
 }
 #ifdef ASB_L2HINTS
-#define ASB_GATHER(ptr) ldg4_hint(ptr, gpol)
+#define ASB_GPOL , gpol
+template <bool HALF>
+__device__ __forceinline__ float4 gather4(const char* p, unsigned long long pol) {
+  if constexpr (HALF) return ldg_h4(p);
+  return ldg4_hint(reinterpret_cast<const float*>(p), pol);
+}
 #else
-#define ASB_GATHER(ptr) ldg4(ptr)
+#define ASB_GPOL
+template <bool HALF>
+__device__ __forceinline__ float4 gather4(const char* p) {
+  if constexpr (HALF) return ldg_h4(p);
+  return ldg4(reinterpret_cast<const float*>(p));
+}
 #endif
 __device__ __forceinline__ void st4_streaming(float* p, float4 v) {
   __stcs(reinterpret_cast<float4*>(p), v);
@@ -154,12 +192,11 @@ template <int GL, int NV>
 __device__ __forceinline__ void load_row_state(const SegParams& p, const DevTable& tb, int seg, int c,
                                                float4 (&w)[NV], float& m) {
   const int nvec = tb.dim >> 2;
-  const float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
   m = p.M[tb.row_off + seg];
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     const int cv = c + q * GL;
-    w[q] = cv < nvec ? *reinterpret_cast<const float4*>(wr + cv * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    w[q] = cv < nvec ? load_w4(p, tb, seg, cv) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -176,7 +213,6 @@ __device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& 
   sq = group_sum<GL>(sq, gmask);
   const float m = m_old + sq / (float)tb.dim;
   const float mult = p.lr / (sqrtf(m) + p.eps);
-  float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
 #pragma unroll
   for (int q = 0; q < NV; ++q) {
     const int cv = c + q * GL;
@@ -186,7 +222,7 @@ __device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& 
       x.y -= mult * g[q].y;
       x.z -= mult * g[q].z;
       x.w -= mult * g[q].w;
-      *reinterpret_cast<float4*>(wr + cv * 4) = x;
+      store_w4(p, tb, seg, cv, x);
     }
   }
   if (c == 0) p.M[tb.row_off + seg] = m;
@@ -210,7 +246,6 @@ __device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTa
     load_row_state<GL, NV>(p, tb, seg, c, w, m_old);
     const float m = m_old + sq / (float)tb.dim;
     const float mult = p.lr / (sqrtf(m) + p.eps);
-    float* wr = p.W + tb.w_base + (long long)seg * tb.dim;
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
       const int cv = c + q * GL;
@@ -220,7 +255,7 @@ __device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTa
         x.y -= mult * g[q].y;
         x.z -= mult * g[q].z;
         x.w -= mult * g[q].w;
-        *reinterpret_cast<float4*>(wr + cv * 4) = x;
+        store_w4(p, tb, seg, cv, x);
       }
     }
     if (c == 0) p.M[tb.row_off + seg] = m;
@@ -297,7 +332,7 @@ __host__ __device__ constexpr int stage_s_ints(int kind) { return (32 / kind_gl(
 #else
 #define ASB_ROWID(x) ((unsigned)(x))
 #endif
-template <bool FWD, int GL, int NV, bool EXACT>
+template <bool FWD, int GL, int NV, bool EXACT, bool HALF>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
   const int kStageX = p.stage_x, kStageS = p.stage_s;
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
@@ -321,14 +356,16 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   // gathered row = gbase + row_id * gstride (bytes): one IMAD.WIDE.U32 per gather
   const char* gbase;
   unsigned gstride;
+  constexpr int VB = HALF ? 8 : 16;  // bytes of one lane's 4 columns
   if constexpr (FWD) {
-    gbase = reinterpret_cast<const char*>(p.W_ro + tb.w_base);
-    gstride = (unsigned)tb.dim * 4u;
+    gbase = HALF ? reinterpret_cast<const char*>(reinterpret_cast<const __half*>(p.W_ro) + tb.w_base)
+                 : reinterpret_cast<const char*>(p.W_ro + tb.w_base);
+    gstride = (unsigned)tb.dim * (HALF ? 2u : 4u);
   } else {
     gbase = reinterpret_cast<const char*>(p.grad + tb.col);
     gstride = (unsigned)p.grad_stride * 4u;
   }
-  gbase += c * 16;
+  gbase += c * VB;
 #ifdef ASB_L2HINTS
   const unsigned long long gpol = l2_policy_last();
 #endif
@@ -400,7 +437,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
           for (int w = 0; w < NV; ++w)
-            v[u][w] = (EXACT || c + w * GL < nvec) ? ASB_GATHER(reinterpret_cast<const float*>(row + w * GL * 16))
+            v[u][w] = (EXACT || c + w * GL < nvec) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       } else {
@@ -410,9 +447,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
           for (int w = 0; w < NV; ++w)
-            v[u][w] = (ok && (EXACT || c + w * GL < nvec))
-                          ? ASB_GATHER(reinterpret_cast<const float*>(row + w * GL * 16))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[u][w] = (ok && (EXACT || c + w * GL < nvec)) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
       if constexpr (GL < 32) {
@@ -525,7 +561,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #ifndef ASB_SEG_MINBLOCKS_BWD
 #define ASB_SEG_MINBLOCKS_BWD ASB_SEG_MINBLOCKS
 #endif
-template <bool FWD>
+template <bool FWD, bool HALF = false>
 __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MINBLOCKS_BWD)
     seg_reduce_kernel(SegParams p) {
   // per warp: [2][stage_x] row ids then [2][stage_s] keys (sized on the host
@@ -543,9 +579,9 @@ __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MIN
 #define ASB_SEG_CASE(K)                                                                  \
   case K:                                                                                \
     if (ex)                                                                              \
-      seg_unit<FWD, kind_gl(K), kind_nv(K), true>(p, tb, t, unit, x, s);                 \
+      seg_unit<FWD, kind_gl(K), kind_nv(K), true, HALF>(p, tb, t, unit, x, s);           \
     else                                                                                 \
-      seg_unit<FWD, kind_gl(K), kind_nv(K), false>(p, tb, t, unit, x, s);                \
+      seg_unit<FWD, kind_gl(K), kind_nv(K), false, HALF>(p, tb, t, unit, x, s);          \
     break;
 #ifdef ASB_ONLY_KIND  // register/spill study builds only
   switch (ASB_ONLY_KIND) {
@@ -569,9 +605,9 @@ __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MIN
     ASB_SEG_CASE(12)
     default:
       if (ex)
-        seg_unit<FWD, 32, 8, true>(p, tb, t, unit, x, s);
+        seg_unit<FWD, 32, 8, true, HALF>(p, tb, t, unit, x, s);
       else
-        seg_unit<FWD, 32, 8, false>(p, tb, t, unit, x, s);
+        seg_unit<FWD, 32, 8, false, HALF>(p, tb, t, unit, x, s);
       break;
   }
 #undef ASB_SEG_CASE
@@ -871,7 +907,9 @@ __device__ __forceinline__ float grid_value(unsigned long long h) {
 }
 
 // W_t[r, d] for one table; s0 = splitmix64(seed) precomputed on the host.
-__global__ void init_table_kernel(float* __restrict__ W, long long rows, int dim, int table_id,
+// The grid values k*2^-12, |k| <= 512, are exact in fp16 too (HALF storage).
+template <bool HALF>
+__global__ void init_table_kernel(void* __restrict__ Wv, long long rows, int dim, int table_id,
                                   unsigned long long s0) {
   const long long nv = rows * (dim >> 2);
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nv;
@@ -885,7 +923,10 @@ __global__ void init_table_kernel(float* __restrict__ W, long long rows, int dim
     x.y = grid_value(dev_splitmix64(s0 ^ (base | (unsigned long long)(d0 + 1))));
     x.z = grid_value(dev_splitmix64(s0 ^ (base | (unsigned long long)(d0 + 2))));
     x.w = grid_value(dev_splitmix64(s0 ^ (base | (unsigned long long)(d0 + 3))));
-    reinterpret_cast<float4*>(W)[q] = x;
+    if constexpr (HALF)
+      reinterpret_cast<uint2*>(Wv)[q] = float4_to_half4(x);
+    else
+      reinterpret_cast<float4*>(Wv)[q] = x;
   }
 }
 

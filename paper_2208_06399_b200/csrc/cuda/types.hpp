@@ -74,6 +74,9 @@ struct SegParams {
   long long out_stride;
   double* loss;  // optional: += 1/2 sum of squares of the pooled rows
   PeerOut peers;
+  // fp16 weight storage (bytes_per_param 2): W holds
+  // __half (W_ro / W reinterpret), fp32 accumulation and update
+  int w_half;
   // backward
   const float* grad;
   long long grad_stride;

@@ -61,13 +61,19 @@ class BenchConfig:
 class EmbeddingShard:
     """One shard (a list of tables) resident on one device (``as_ctx``)."""
 
-    def __init__(self, tables: Sequence[TableDesc], batch_size: int, device: int = 0, weight_seed: int = 0):
+    def __init__(self, tables: Sequence[TableDesc], batch_size: int, device: int = 0, weight_seed: int = 0,
+                 weights: str = "fp32"):
+        """weights: "fp32" or "fp16" (as_create_ex AS_WEIGHTS_FP16: bytes_per_param 2 storage,
+        fp32 accumulation and update)."""
         self.tables = list(tables)
         self.batch_size = int(batch_size)
         self.device = int(device)
+        if weights not in ("fp32", "fp16"):
+            raise ValueError(f"weights must be 'fp32' or 'fp16', got {weights!r}")
+        self.weights = weights
         h = C.c_void_p()
-        check(lib().as_create(self.device, specs_to_c(self.tables), len(self.tables), self.batch_size,
-                              weight_seed, C.byref(h)))
+        check(lib().as_create_ex(self.device, specs_to_c(self.tables), len(self.tables), self.batch_size,
+                                 weight_seed, 1 if weights == "fp16" else 0, C.byref(h)))
         self._h = h
         self.sum_dim = sum(t.dim for t in self.tables)
         self.cols = np.cumsum([0] + [t.dim for t in self.tables])[:-1].tolist()

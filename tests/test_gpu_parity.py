@@ -131,6 +131,7 @@ def test_long_bags_hot_rows_empty_tables(P, oracle, cuda, dim):
     # exactly one / two chunks and chunk-1 / chunk+1 exercise every carry case
     est = 4.0 * dim * (20000 + 4 * 2048 + 5000 + 50 * B)
     target = max(2048.0, min(131072.0, est / (148.0 * 24.0)))
+    target = min(target, 262144.0 / (8 if dim == 16 else 1))  # 256 KB per warp unit of 32/GL chunks
     chunk = max(32, min(8192, int(target / (dim * 4.0)) // 32 * 32))
     lens = [
         np.array([0, 20000, 1, 0, 0, chunk, chunk, 2 * chunk + 1] + [3] * (B - 8)),
@@ -458,3 +459,40 @@ def test_fused_exchange_symmetric_memory_world1(tmp_path):
                MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29000 + os.getpid() % 1000))
     r = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("dims", [(4, 16, 32, 64), (128, 132, 256, 512)])
+def test_fp16_weight_storage(P, oracle, cuda, dims):
+    """AS_WEIGHTS_FP16 (bytes_per_param 2). Forward: bit-exact
+    (the grid init k*2^-12, |k| <= 512, is exact in fp16 and accumulation is
+    fp32). Backward: the fp32 update rounded to nearest fp16, so the updated
+    rows match the fp64 oracle within half an fp16 ulp (2^-11 relative) plus
+    the fp32 bound; momentum stays fp32 (1e-5)."""
+    pool = P.generate_pool(4, len(dims), P.GeneratorConfig(hash_size_max=4e4, pooling_mean_target=25.0))
+    for t, d in zip(pool, dims):
+        t.dim = d
+    B, seed = 256, 6
+    wl = P.generate_workload(3, pool, B)
+    st = streams_of(wl, pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed, weights="fp16") as sh:
+        assert sh.info().weight_bytes == 2
+        sh.load(st)
+        sh.forward()
+        pooled = sh.read_pooled()
+        ref = oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed)
+        assert np.array_equal(pooled.astype(np.float64), ref)
+        sh.backward(None, LR, EPS)
+        for t, tab in enumerate(pool):
+            r = oracle.backward_adagrad_f64(to_oracle_tables([tab])[0], B, *st[t], pooled, sh.cols[t], LR, EPS,
+                                            wseed=seed)
+            if len(r["rows"]) == 0:
+                continue
+            w = sh.read_rows(t, r["rows"]).astype(np.float64)
+            w_old = weight_rows(seed, tab.id, r["rows"], tab.dim).astype(np.float64)
+            scale = np.maximum(np.abs(w_old), np.abs(w_old - r["w"]))
+            tol = 2.0 ** -11 * np.abs(r["w"]) * 1.001 + 1e-5 * scale + 2.0 ** -24
+            err = np.abs(w - r["w"])
+            assert (err <= tol).all(), f"table {tab.id}: fp16 rows off by {float((err / tol).max()):.3g}x tolerance"
+            assert np.array_equal(w, w.astype(np.float16).astype(np.float64))  # stored values are fp16
+            ok, worst = fp_close(sh.read_momentum(t, r["rows"]), r["m"])
+            assert ok, f"table {tab.id}: momentum off by {worst:.3g}x tolerance"
