@@ -56,6 +56,10 @@ def build_workload(P, name):
         return tables, 65536, "cfg3: generate_pool(0,100,dims {32,64,128,256}), batch 65536"
     if name == "cfg4":
         return P.generate_pool(0, 856), 65536, "cfg4: generate_pool(0,856) dims {16,32}, batch 65536"
+    if name == "cfg5":
+        # unseen-table transfer: the AutoShard-RL plan is trained on tables 0..427 only
+        return (P.generate_pool(0, 856, P.GeneratorConfig(dim_choices=(64, 128, 192, 256))), 131072,
+                "cfg5: generate_pool(0,856,dims {64,128,192,256}), batch 131072 (RL trained on tables 0..427)")
     if name == "cfg1":
         tables = P.generate_pool(0, 10, P.GeneratorConfig(dim_choices=(64,), pooling_mean_target=20.0))
         return tables, 512, "cfg1: generate_pool(0,10,dim 64,pooling 20), batch 512"

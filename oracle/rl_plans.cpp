@@ -12,6 +12,10 @@
 // writes <out_prefix>.assignment (one line, n_target shard ids) and
 // <out_prefix>.ckpt (the reference checkpoint, ASHCKPT1).
 //
+// TRAIN_RANGE=a:b: train on subsets of pool tables [a, b) instead of
+// [n_target, n_pool) — BASELINE cfg 5 (856 tables, 50% unseen): n_pool =
+// n_target = 856, TRAIN_RANGE=0:428.
+//
 // MARGINALS=<file>: train against B200-MEASURED costs
 // instead of the analytic SIM (tools/measure_marginals.py writes the file:
 // c0, rho and per-table marginals w_t = measured one-table time - c0). Every
@@ -58,7 +62,13 @@ int main(int argc, char** argv) {
   const auto pool = generate_pool(0, n_pool, gcfg);
   const Workload wl = generate_workload(0, pool, batch);
   const std::vector<TableDesc> target(pool.begin(), pool.begin() + n_target);
-  const std::vector<TableDesc> train_pool(pool.begin() + n_target, pool.end());
+  int tr_lo = n_target, tr_hi = n_pool;
+  if (const char* r = std::getenv("TRAIN_RANGE")) std::sscanf(r, "%d:%d", &tr_lo, &tr_hi);
+  if (tr_lo < 0 || tr_hi > n_pool || tr_lo >= tr_hi) {
+    std::fprintf(stderr, "bad TRAIN_RANGE %d:%d\n", tr_lo, tr_hi);
+    return 2;
+  }
+  const std::vector<TableDesc> train_pool(pool.begin() + tr_lo, pool.begin() + tr_hi);
   const NormStats norm = compute_norm_stats(train_pool, wl);
   const FeatureMask mask{};
   SimParams sim{};

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--measure", type=int, default=10)
     ap.add_argument("--trim", type=int, default=2)
+    ap.add_argument("--weights", choices=["fp32", "fp16"], default="fp32")
+    ap.add_argument("--plans", default="", help="comma list of plan names to measure (default: all)")
     args = ap.parse_args()
 
     tables, B, desc = bench.build_workload(P, args.workload)
@@ -47,16 +49,45 @@ def main():
         plans[name] = P.greedy_shard(task, kind)
     for s in range(args.random_seeds):
         plans[f"random-{s}"] = P.random_shard(task, s)
-    rl = os.path.join(ROOT, "plans", f"{args.workload}_autoshard_rl.assignment")
-    if os.path.exists(rl):
-        a = [int(x) for x in open(rl).read().split()]
-        if len(a) == len(tables):
-            plans["autoshard-rl"] = P.ShardingPlan(a)
+    for tag, fname in (("autoshard-rl", f"{args.workload}_autoshard_rl"),
+                       ("autoshard-rl", f"{args.workload}_k{K}_autoshard_rl"),
+                       ("autoshard-rl-gpu", f"{args.workload}_autoshard_rl_gpu")):
+        rl = os.path.join(ROOT, "plans", fname + ".assignment")
+        if os.path.exists(rl):
+            a = [int(x) for x in open(rl).read().split()]
+            if len(a) == len(tables) and max(a) < K:
+                plans[tag] = P.ShardingPlan(a)
+    # LPT greedy over GPU-MEASURED per-table costs (tools/measure_marginals.py), the
+    # planners.hpp:73-107 algorithm with the analytic cost replaced by the measurement
+    mj = os.path.join(ROOT, "plans", f"{args.workload}_gpu_marginals.json")
+    if os.path.exists(mj):
+        ms = json.load(open(mj))["single_ms"]
+        if all(str(t.id) in ms for t in tables):
+            order = sorted(range(len(tables)), key=lambda i: (-ms[str(tables[i].id)], tables[i].id))
+            load, used, a = [0.0] * K, [0] * K, [0] * len(tables)
+            for i in order:
+                fits = [k for k in range(K) if used[k] + tables[i].size_bytes() <= task.mem_budget[k]] or list(range(K))
+                k = min(fits, key=lambda k: (load[k], k))
+                a[i] = k
+                load[k] += ms[str(tables[i].id)]
+                used[k] += tables[i].size_bytes()
+            plans["measured-greedy"] = P.ShardingPlan(a)
+    if args.plans:
+        keep = set(args.plans.split(","))
+        plans = {k: v for k, v in plans.items() if k in keep or k.split("-")[0] in keep}
     bench_cfg = P.BenchConfig(warmup=args.warmup, measure=args.measure, trim=args.trim)
     res = {}
     for name, plan in plans.items():
         t0 = time.time()
-        costs = P.measure_plan(plan, task, wl, bench_cfg)
+        if args.weights == "fp32":
+            costs = P.measure_plan(plan, task, wl, bench_cfg)
+        else:  # same protocol shard by shard, fp16 table storage
+            costs = []
+            for members in plan.shard_member_indices(task):
+                tabs = [tables[i] for i in members]
+                with P.EmbeddingShard(tabs, B, weight_seed=0, weights=args.weights) as sh:
+                    sh.load([(wl.find(t.id).offsets, wl.find(t.id).indices) for t in tabs])
+                    costs.append(sh.measure(args.warmup, args.measure, args.trim))
         res[name] = {"assignment": plan.assignment, "shard_ms": costs, "max_ms": max(costs),
                      "balance": P.degree_of_balance(costs), "feasible": plan.feasible(task),
                      "wall_s": round(time.time() - t0, 1)}
@@ -67,7 +98,7 @@ def main():
     for k, v in res.items():
         v["speedup_vs_random_mean"] = rnd_mean / v["max_ms"]
         v["speedup_vs_lookup_greedy"] = res["lookup-greedy"]["max_ms"] / v["max_ms"]
-    out = {"workload": args.workload, "desc": desc, "shards": K, "batch": B,
+    out = {"workload": args.workload, "desc": desc, "shards": K, "batch": B, "weights": args.weights,
            "budget_rule": "1.6 x total / K (SPEC.md:620), bytes_per_param 2",
            "protocol": f"W={args.warmup} B={args.measure} R={args.trim}, L2 flushed, one shard at a time on 1 GPU",
            "random_max_ms_mean": rnd_mean, "plans": res}
