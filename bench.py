@@ -279,6 +279,9 @@ def main():
                     help="cfg1|cfg2|cfg2u|cfg3|cfg4 (auto: cfg2 at N=1, cfg4 at N>1)")
     ap.add_argument("--weights", choices=["fp32", "fp16"], default="fp32",
                     help="table storage (fp16 = bytes_per_param 2, as_create_ex AS_WEIGHTS_FP16; fp32 accumulation)")
+    ap.add_argument("--plan-shard", type=int, default=-1,
+                    help="N=1: run only this shard of the --plan-k GPU plan (AutoShard-RL if present)")
+    ap.add_argument("--plan-k", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
@@ -299,9 +302,17 @@ def main():
 
     import paper_2208_06399_b200 as P
 
+    # ASB_TEST_ONE_GPU=1 (functional test of the N>1 path on a 1-GPU box only):
+    # every rank on cuda:0, gloo instead of NCCL. Never used for timings.
+    one_gpu = os.environ.get("ASB_TEST_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     tables_all, B, wdesc = build_workload(P, wname)
     if world > 1:
@@ -311,6 +322,13 @@ def main():
         task = P.ShardingTask(tables_all, world, budget)
         plan, plan_name = bench_plan(P, task, wname, world)
         mine = [t for t, k in zip(tables_all, plan.assignment) if k == rank]
+    elif args.plan_shard >= 0:
+        # one shard of the K-GPU plan on this GPU (the per-GPU work of the K-GPU
+        # run; the K-GPU box time is the max over its shards)
+        task = P.ShardingTask(tables_all, args.plan_k, [int(180e9)] * args.plan_k)
+        plan, plan_name = bench_plan(P, task, wname, args.plan_k)
+        plan_name = f"shard {args.plan_shard} of {args.plan_k}: {plan_name}"
+        mine = [t for t, k in zip(tables_all, plan.assignment) if k == args.plan_shard]
     else:
         plan_name = "single shard"
         mine = list(tables_all)
@@ -339,7 +357,8 @@ def main():
                 exchange = "fused: pooled rows stored into the sample owners' symmetric-memory receive buffers by the " \
                            "forward kernel + device barrier; backward: NCCL all_to_all_single"
             except Exception as e:  # noqa: BLE001
-                exchange = f"NCCL all_to_all_single both ways (symmetric memory unavailable: {type(e).__name__})"
+                exchange = (f"NCCL all_to_all_single both ways (symmetric memory unavailable: "
+                            f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''})")
         if exch is None:
             exch = PooledExchange(lay, rank, device="cuda")
             exchange = exchange or "NCCL all_to_all_single both ways"

@@ -145,10 +145,6 @@ class FusedPooledExchange:
 
         self.L, self.rank, self.group = layout, rank, group
         group = group or dist.group.WORLD
-        try:
-            symm_mem.enable_symm_mem_for_group(group.group_name)
-        except Exception:
-            pass
         n = layout.rows_per_rank * sum(layout.shard_dims)
         self.recv_buf = symm_mem.empty(n, dtype=torch.float32, device=device)
         self.hdl = symm_mem.rendezvous(self.recv_buf, group)
