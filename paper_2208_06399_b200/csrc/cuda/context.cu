@@ -52,13 +52,24 @@ struct DeviceGuard {
 
 // Lane layout of a table: NV = vec float4 per lane when the row is wide enough
 // for >= 8 lanes (one warp instruction then gathers 32/GL rows), else 1.
-int kind_for_dim(int dim, int vec) {
+int kind_for_dim(int dim, int vec, bool half) {
   const int nvec = dim / 4;
   auto pow2ceil = [](int x) {
     int p = 1;
     while (p < x) p <<= 1;
     return p;
   };
+  // fp16 tables: PAIRED layouts, one 16-B load (8 halves) per lane and slot pair
+  if (half && dim % 8 == 0 && dim >= 64) {
+    const int n8 = dim / 8;
+    if (n8 <= 32) {
+      const int gl = pow2ceil(n8);
+      for (int k = 0; k < kNumKinds; ++k)
+        if (kind_gl(k) == gl && kind_nv(k) == 2) return k;
+    }
+    if (n8 <= 64) return 7;
+    return 8;
+  }
   if (vec >= 2 && nvec >= 16 && nvec <= 32 * vec) {
     const int nv = (vec >= 4 && nvec >= 32) ? 4 : 2;
     const int gl = std::min(32, pow2ceil((nvec + nv - 1) / nv));
@@ -211,10 +222,12 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     d.dim = s.dim;
     d.col = static_cast<int>(sum_dim_);
     d.table_id = s.id;
-    d.kind = kind_for_dim(s.dim, vec_);
+    d.kind = kind_for_dim(s.dim, vec_, w_half_);
     d.chunk_len = chunk_len_for(s.dim, 131072.0);
     total_rows_ += s.hash_size;
-    w_off += s.hash_size * s.dim;
+    // every table starts 128-B aligned (fp32; 64 B for fp16): 16-B vector rows,
+    // and the paired fp16 layouts' 16-B loads, never straddle a table start
+    w_off += (s.hash_size * s.dim + 31) / 32 * 32;
     sum_dim_ += s.dim;
     max_dim_ = std::max(max_dim_, s.dim);
   }
@@ -284,8 +297,8 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
 
   // K6: weights from the counter hash, momentum zero.
   const unsigned long long s0 = splitmix64(seed_);
-  int64_t off = 0;
   for (int t = 0; t < n; ++t) {
+    const int64_t off = htabs_[t].w_base;
     const long long nv = specs_[t].hash_size * (specs_[t].dim / 4);
     const unsigned grid = static_cast<unsigned>(std::min<long long>((nv + 255) / 256, 148LL * 64));
     if (w_half_)
@@ -293,7 +306,6 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
                                              specs_[t].id, s0);
     else
       init_table_kernel<false><<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
-    off += specs_[t].hash_size * specs_[t].dim;
   }
   cuda_check(cudaGetLastError(), "init_table_kernel");
   cuda_check(cudaMemset(M_, 0, sizeof(float) * static_cast<size_t>(total_rows_)), "momentum init");

@@ -94,6 +94,16 @@ __device__ __forceinline__ uint2 float4_to_half4(float4 v) {
   const __half2 b = __floats2half2_rn(v.z, v.w);
   return make_uint2(*reinterpret_cast<const unsigned*>(&a), *reinterpret_cast<const unsigned*>(&b));
 }
+// 8 halves (16 B) -> two float4; zeros when !ok
+__device__ __forceinline__ void gather8h(float4& a, float4& b, bool ok, const char* p) {
+  if (ok) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(p));
+    a = half4_to_float4(make_uint2(r.x, r.y));
+    b = half4_to_float4(make_uint2(r.z, r.w));
+  } else {
+    a = b = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
 __device__ __forceinline__ float4 ldg_h4(const char* p) {
   return half4_to_float4(__ldg(reinterpret_cast<const uint2*>(p)));
 }
@@ -171,16 +181,26 @@ __device__ __forceinline__ float* pooled_row(float* out, long long stride, const
   return peers.base[q] + (long long)(b - q * peers.rows) * stride;
 }
 
+// Column group (4 columns) held in slot w of lane c. Standard layouts stride
+// the slots by GL; PAIRED layouts (fp16 tables: one 16-B load = 8 halves per
+// lane) hold two adjacent groups per load: slots 2k, 2k+1 = groups
+// 2(c + k*GL), 2(c + k*GL) + 1.
+template <int GL, bool PAIR>
+__device__ __forceinline__ int colv(int c, int w) {
+  if constexpr (PAIR) return 2 * (c + (w >> 1) * GL) + (w & 1);
+  return c + w * GL;
+}
+
 // Segment epilogues, executed by the GL lanes of one group.
 // forward : pooled[bag, col_t + :] = v   (+ loss 1/2|v|^2)
-template <int GL, int NV>
+template <int GL, int NV, bool PAIR = false>
 __device__ __forceinline__ void store_pooled(const SegParams& p, const DevTable& tb, int seg, const float4 (&v)[NV],
                                              int c, float& loss_acc) {
   const int nvec = tb.dim >> 2;
   float* o = pooled_row(p.out, p.out_stride, p.peers, seg) + tb.col;
 #pragma unroll
   for (int w = 0; w < NV; ++w) {
-    const int cv = c + w * GL;
+    const int cv = colv<GL, PAIR>(c, w);
     if (cv < nvec) {
       st4_streaming(o + cv * 4, v[w]);
       loss_acc += f4dot(v[w]);
@@ -275,13 +295,13 @@ __device__ __forceinline__ void finish_segment(const SegParams& p, const DevTabl
   }
 }
 
-template <int GL, int NV>
+template <int GL, int NV, bool PAIR = false>
 __device__ __forceinline__ void store_carry(const SegParams& p, int chunk, int which, int nvec, int c,
                                             const float4 (&v)[NV]) {
   float* dst = p.carry + ((long long)chunk * 2 + which) * p.carry_stride;
 #pragma unroll
   for (int w = 0; w < NV; ++w) {
-    const int cv = c + w * GL;
+    const int cv = colv<GL, PAIR>(c, w);
     if (cv < nvec) *reinterpret_cast<float4*>(dst + cv * 4) = v[w];
   }
 }
@@ -332,7 +352,7 @@ __host__ __device__ constexpr int stage_s_ints(int kind) { return (32 / kind_gl(
 #else
 #define ASB_ROWID(x) ((unsigned)(x))
 #endif
-template <bool FWD, int GL, int NV, bool EXACT, bool HALF>
+template <bool FWD, int GL, int NV, bool EXACT, bool HALF, bool PAIR_>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
   const int kStageX = p.stage_x, kStageS = p.stage_s;
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
@@ -357,6 +377,9 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const char* gbase;
   unsigned gstride;
   constexpr int VB = HALF ? 8 : 16;  // bytes of one lane's 4 columns
+  // fp16 rows with dim % 8 == 0 get PAIRED layouts (kind_for_dim): one 16-B
+  // load = 8 halves = slots w, w+1
+  constexpr bool PAIR = FWD && HALF && (NV % 2 == 0) && PAIR_;
   if constexpr (FWD) {
     gbase = HALF ? reinterpret_cast<const char*>(reinterpret_cast<const __half*>(p.W_ro) + tb.w_base)
                  : reinterpret_cast<const char*>(p.W_ro + tb.w_base);
@@ -365,7 +388,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     gbase = reinterpret_cast<const char*>(p.grad + tb.col);
     gstride = (unsigned)p.grad_stride * 4u;
   }
-  gbase += c * VB;
+  gbase += PAIR ? c * 16 : c * VB;
 #ifdef ASB_L2HINTS
   const unsigned long long gpol = l2_policy_last();
 #endif
@@ -436,9 +459,15 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
         for (int u = 0; u < U; ++u) {
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
-          for (int w = 0; w < NV; ++w)
-            v[u][w] = (EXACT || c + w * GL < nvec) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (PAIR) {
+            for (int w = 0; w < NV; w += 2)
+              gather8h(v[u][w], v[u][w + 1], EXACT || colv<GL, true>(c, w) < nvec, row + (w >> 1) * GL * 16);
+          } else {
+#pragma unroll
+            for (int w = 0; w < NV; ++w)
+              v[u][w] = (EXACT || c + w * GL < nvec) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
       } else {
 #pragma unroll
@@ -446,9 +475,15 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           const bool ok = m0 + u < nval;
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
 #pragma unroll
-          for (int w = 0; w < NV; ++w)
-            v[u][w] = (ok && (EXACT || c + w * GL < nvec)) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
-                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          if constexpr (PAIR) {
+            for (int w = 0; w < NV; w += 2)
+              gather8h(v[u][w], v[u][w + 1], ok && (EXACT || colv<GL, true>(c, w) < nvec), row + (w >> 1) * GL * 16);
+          } else {
+#pragma unroll
+            for (int w = 0; w < NV; ++w)
+              v[u][w] = (ok && (EXACT || c + w * GL < nvec)) ? gather4<HALF>(row + w * GL * VB ASB_GPOL)
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
       }
       if constexpr (GL < 32) {
@@ -463,11 +498,11 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             const int s = gs[m0 + u];
             const bool split = s == prev_seg;
             if (endu && split) {
-              store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
+              store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
               if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
             }
             if constexpr (FWD) {
-              if (endu && !split) store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
+              if (endu && !split) store_pooled<GL, NV, PAIR>(p, tb, s, acc, c, loss_acc);
             } else {
               adagrad_row_pred<GL, NV>(p, tb, s, acc, c, endu && !split);
             }
@@ -507,10 +542,10 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             const int s = gs[m0 + e];
             if (s == prev_seg) {
               // completes a segment that began in an earlier chunk -> fixup
-              store_carry<GL, NV>(p, chunk, 0, nvec, c, acc);
+              store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
               if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
             } else if constexpr (FWD) {
-              store_pooled<GL, NV>(p, tb, s, acc, c, loss_acc);
+              store_pooled<GL, NV, PAIR>(p, tb, s, acc, c, loss_acc);
             } else {
 #ifdef ASB_ABLATE_EPILOGUE  // ablation builds only: write g, skip the row update
               if (c == 0) p.M[tb.row_off + s] = acc[0].x;
@@ -540,7 +575,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   // The chunk's last segment continues into the next chunk: hand the partial on.
   if (live && j_hi < t_hi) {
     const int sl = __ldg(p.seg + j_hi - 1);
-    if (__ldg(p.seg + j_hi) == sl) store_carry<GL, NV>(p, chunk, sl == prev_seg ? 0 : 1, nvec, c, acc);
+    if (__ldg(p.seg + j_hi) == sl) store_carry<GL, NV, PAIR>(p, chunk, sl == prev_seg ? 0 : 1, nvec, c, acc);
   }
   if constexpr (FWD) {
     if (p.loss) {
@@ -561,6 +596,19 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #ifndef ASB_SEG_MINBLOCKS_BWD
 #define ASB_SEG_MINBLOCKS_BWD ASB_SEG_MINBLOCKS
 #endif
+// fp16 forward: the paired 16-B layout for rows with dim % 8 == 0 (16-B
+// aligned), the 8-B layout otherwise
+template <bool FWD, int GL, int NV, bool EXACT, bool HALF>
+__device__ __forceinline__ void seg_unit_d(const SegParams& p, const DevTable& tb, int t, int unit, int* x, int* s) {
+  if constexpr (FWD && HALF && NV % 2 == 0) {
+    if ((tb.dim & 7) == 0) {
+      seg_unit<FWD, GL, NV, EXACT, HALF, true>(p, tb, t, unit, x, s);
+      return;
+    }
+  }
+  seg_unit<FWD, GL, NV, EXACT, HALF, false>(p, tb, t, unit, x, s);
+}
+
 template <bool FWD, bool HALF = false>
 __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MINBLOCKS_BWD)
     seg_reduce_kernel(SegParams p) {
@@ -579,9 +627,9 @@ __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MIN
 #define ASB_SEG_CASE(K)                                                                  \
   case K:                                                                                \
     if (ex)                                                                              \
-      seg_unit<FWD, kind_gl(K), kind_nv(K), true, HALF>(p, tb, t, unit, x, s);           \
+      seg_unit_d<FWD, kind_gl(K), kind_nv(K), true, HALF>(p, tb, t, unit, x, s);         \
     else                                                                                 \
-      seg_unit<FWD, kind_gl(K), kind_nv(K), false, HALF>(p, tb, t, unit, x, s);          \
+      seg_unit_d<FWD, kind_gl(K), kind_nv(K), false, HALF>(p, tb, t, unit, x, s);        \
     break;
 #ifdef ASB_ONLY_KIND  // register/spill study builds only
   switch (ASB_ONLY_KIND) {
@@ -605,9 +653,9 @@ __global__ void __launch_bounds__(256, FWD ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MIN
     ASB_SEG_CASE(12)
     default:
       if (ex)
-        seg_unit<FWD, 32, 8, true, HALF>(p, tb, t, unit, x, s);
+        seg_unit_d<FWD, 32, 8, true, HALF>(p, tb, t, unit, x, s);
       else
-        seg_unit<FWD, 32, 8, false, HALF>(p, tb, t, unit, x, s);
+        seg_unit_d<FWD, 32, 8, false, HALF>(p, tb, t, unit, x, s);
       break;
   }
 #undef ASB_SEG_CASE
