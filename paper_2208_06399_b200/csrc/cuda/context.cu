@@ -115,6 +115,20 @@ __global__ void gather_rows_kernel(const void* __restrict__ src, int half, long 
   }
 }
 
+// Device side of the staging split: int64 lookups copied raw
+// are narrowed to int32 rows on the GPU and validated against [0, hash) with
+// load_workload's check (workload_io.hpp:216-241); the first bad entry wins
+// through the same (table, check, entry) key the host validation uses.
+__global__ void narrow_validate_kernel(const long long* __restrict__ src, int* __restrict__ dst, long long n,
+                                       long long hash, unsigned long long key_base,
+                                       unsigned long long* __restrict__ err) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const long long v = src[j];
+    dst[j] = (int)v;
+    if ((unsigned long long)v >= (unsigned long long)hash) atomicMin(err, key_base | (unsigned long long)j);
+  }
+}
+
 constexpr int kBlock = 256;
 constexpr int kWarpsPerBlock = kBlock / 32;
 
@@ -254,8 +268,18 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
                "pinned staging");
     cuda_check(cudaEventCreateWithFlags(&sl.copied, cudaEventDisableTiming), "event");
     cuda_check(cudaEventCreateWithFlags(&sl.retired, cudaEventDisableTiming), "event");
+    sl.d_err = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
+    cuda_check(cudaHostAlloc(&sl.h_err, sizeof(unsigned long long), cudaHostAllocDefault), "pinned error key");
   }
+  if (const char* e = std::getenv("ASB_RAW_EIGHTHS")) raw_eighths_ = std::max(0, std::min(8, std::atoi(e)));
   cuda_check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "copy stream");
+  {
+    int lo = 0, hi = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+    // GPU narrowing of staged pieces: highest priority, so its small CTAs take
+    // the first free SM slots inside a running step instead of queueing behind it
+    cuda_check(cudaStreamCreateWithPriority(&narrow_, cudaStreamNonBlocking, hi), "narrow stream");
+  }
   err_ = static_cast<unsigned long long*>(dalloc(sizeof(unsigned long long)));
   loss_ = static_cast<double*>(dalloc(sizeof(double)));
   cuda_check(cudaHostAlloc(&h_loss_, sizeof(double), cudaHostAllocDefault), "pinned loss");
@@ -326,12 +350,16 @@ EmbContext::~EmbContext() {
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
   if (copy_) cudaStreamDestroy(copy_);
+  if (narrow_) cudaStreamDestroy(narrow_);
   for (Slot& sl : slots_) {
     if (sl.job.joinable()) sl.job.join();
     if (sl.copied) cudaEventDestroy(sl.copied);
     if (sl.retired) cudaEventDestroy(sl.retired);
     if (sl.h_idx32) cudaFreeHost(sl.h_idx32);
     if (sl.h_off32) cudaFreeHost(sl.h_off32);
+    if (sl.h_err) cudaFreeHost(sl.h_err);
+    for (auto e : sl.raw_ev) cudaEventDestroy(e);
+    if (sl.narrowed) cudaEventDestroy(sl.narrowed);
   }
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
@@ -563,18 +591,61 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   sl.err_val = 0;
   sl.staged = true;
   sl.seq = ++stage_seq_;
-  // background job: narrow + validate + H2D, per table piece, on the pool
-  std::vector<std::array<int64_t, 3>> tasks;  // {table, begin, end}; begin = -1: offsets
+  // background job: narrow + validate + H2D, per table piece, on the pool.
+  // raw_eighths_/8 of the index pieces of PINNED tables go host->device as
+  // int64 and are narrowed + validated on the GPU (narrow_validate_kernel):
+  // host memory bandwidth (narrowing) and PCIe (copies) then both work.
+  std::vector<std::array<int64_t, 4>> tasks;  // {table, begin, end, raw offset or -1}; begin = -1: offsets
+  int64_t raw_n = 0, piece = 0;
   for (int t = 0; t < T_; ++t) {
-    tasks.push_back({t, -1, 0});
-    for (int64_t b = 0; b < n_idx[t]; b += kNarrowChunk) tasks.push_back({t, b, std::min(n_idx[t], b + kNarrowChunk)});
+    tasks.push_back({t, -1, 0, -1});
+    bool pinned = false;
+    if (raw_eighths_ > 0 && n_idx[t] > 0) {
+      cudaPointerAttributes a{};
+      pinned = cudaPointerGetAttributes(&a, indices[t]) == cudaSuccess && a.type == cudaMemoryTypeHost;
+      (void)cudaGetLastError();
+    }
+    for (int64_t b = 0; b < n_idx[t]; b += kNarrowChunk, ++piece) {
+      const int64_t e = std::min(n_idx[t], b + kNarrowChunk);
+      const bool raw = pinned && (piece % 8) < raw_eighths_;
+      tasks.push_back({t, b, e, raw ? raw_n : -1});
+      if (raw) raw_n += e - b;
+    }
   }
+  if (raw_n > sl.raw_cap) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    if (sl.d_raw) {
+      auto it = std::find(allocs_.begin(), allocs_.end(), (void*)sl.d_raw);
+      if (it != allocs_.end()) allocs_.erase(it);
+      cudaFree(sl.d_raw);
+    }
+    sl.raw_cap = raw_n + raw_n / 8;
+    sl.d_raw = static_cast<long long*>(dalloc(sizeof(long long) * sl.raw_cap));
+  }
+  sl.raw_used = raw_n > 0;
+  {
+    int64_t n_raw_tasks = 0;
+    for (auto& tk : tasks) n_raw_tasks += tk[3] >= 0;
+    while ((int64_t)sl.raw_ev.size() < n_raw_tasks) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      sl.raw_ev.push_back(e);
+    }
+    if (!sl.narrowed) cuda_check(cudaEventCreateWithFlags(&sl.narrowed, cudaEventDisableTiming), "event");
+    int64_t r = 0;
+    for (auto& tk : tasks)
+      if (tk[3] >= 0) tk[3] |= (r++) << 40;  // event index in the high bits
+  }
+  sl.src_idx.assign(indices, indices + T_);
   std::vector<const int64_t*> off(offsets, offsets + T_), idx(indices, indices + T_);
   Slot* sp = &sl;
   const int dev = device_;
   sl.job = std::thread([this, sp, dev, tasks = std::move(tasks), off = std::move(off), idx = std::move(idx)] {
     try {
       cudaSetDevice(dev);
+      if (sp->raw_used) {  // the reset precedes every narrowing kernel (narrow_ waits on copy_ events)
+        cuda_check(cudaMemsetAsync(sp->d_err, 0xff, sizeof(unsigned long long), copy_), "error key");
+      }
       std::mutex emu;
       auto report = [&](int t, int kind, int64_t entry, int64_t value) {
         const unsigned long long key =
@@ -602,6 +673,18 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
           cuda_check(cudaMemcpyAsync(sp->d_off32 + (int64_t)t * B_, dst, sizeof(int) * (t == T_ - 1 ? B_ + 1 : B_),
                                      cudaMemcpyHostToDevice, copy_),
                      "offsets H2D");
+        } else if (tasks[k][3] >= 0) {  // raw: int64 H2D, narrowed + validated on the GPU
+          const int64_t b = tasks[k][1], e = tasks[k][2];
+          long long* raw = sp->d_raw + (tasks[k][3] & ((1LL << 40) - 1));
+          cudaEvent_t ev = sp->raw_ev[tasks[k][3] >> 40];
+          cuda_check(cudaMemcpyAsync(raw, idx[t] + b, sizeof(long long) * (e - b), cudaMemcpyHostToDevice, copy_),
+                     "indices H2D (raw)");
+          cuda_check(cudaEventRecord(ev, copy_), "raw copied");
+          cuda_check(cudaStreamWaitEvent(narrow_, ev, 0), "narrow wait");
+          narrow_validate_kernel<<<(unsigned)std::min<int64_t>((e - b + 255) / 256, 1184), 256, 0, narrow_>>>(
+              raw, sp->d_idx32 + d.idx_off + b, e - b, d.hash,
+              ((unsigned long long)t << 42) | (3ull << 40) | (unsigned long long)b, sp->d_err);
+          cuda_check(cudaGetLastError(), "narrow_validate_kernel");
         } else {
           const int64_t b = tasks[k][1], e = tasks[k][2];
           const int64_t* src = idx[t];
@@ -619,6 +702,12 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
                      "indices H2D");
         }
       });
+      if (sp->raw_used) {
+        cuda_check(cudaEventRecord(sp->narrowed, narrow_), "narrowed");
+        cuda_check(cudaStreamWaitEvent(copy_, sp->narrowed, 0), "join narrow");
+        cuda_check(cudaMemcpyAsync(sp->h_err, sp->d_err, sizeof(unsigned long long), cudaMemcpyDeviceToHost, copy_),
+                   "error key D2H");
+      }
       cuda_check(cudaEventRecord(sp->copied, copy_), "copied");
     } catch (...) {
       sp->job_error = std::current_exception();
@@ -640,6 +729,14 @@ void EmbContext::commit(cudaStream_t s) {
     auto e = sl.job_error;
     sl.job_error = nullptr;
     std::rethrow_exception(e);
+  }
+  if (sl.raw_used) {  // the GPU-validated pieces: wait for their first-error key
+    cuda_check(cudaEventSynchronize(sl.copied), "staged batch");
+    const unsigned long long dk = *sl.h_err;
+    if (dk < sl.err_key) {
+      sl.err_key = dk;
+      sl.err_val = sl.src_idx[dk >> 42][dk & ((1ull << 40) - 1)];
+    }
   }
   if (sl.err_key != ~0ull) {
     const int t = static_cast<int>(sl.err_key >> 42);

@@ -100,6 +100,14 @@ class EmbContext {
     std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
     std::vector<int> utab;
     int64_t L = 0, nch = 0, nun = 0, n_tma_units = 0;
+    long long* d_raw = nullptr;  // int64 pieces narrowed on the GPU
+    int64_t raw_cap = 0;
+    bool raw_used = false;
+    unsigned long long* d_err = nullptr;  // first GPU validation error key
+    unsigned long long* h_err = nullptr;  // pinned copy
+    std::vector<const int64_t*> src_idx;  // caller's index arrays (error value lookup)
+    std::vector<cudaEvent_t> raw_ev;       // per raw piece: its H2D landed
+    cudaEvent_t narrowed = nullptr;        // every GPU-narrowed piece done
     std::vector<int> sort_meta;  // hist CTA -> table | hist CTA -> chunk | per pass: tile -> table
     int64_t tile_tab_off[kMaxSortPasses] = {0, 0, 0, 0};
     int64_t pass_tiles[kMaxSortPasses] = {0, 0, 0, 0};
@@ -118,6 +126,7 @@ class EmbContext {
   int cur_slot_ = -1;
   uint64_t stage_seq_ = 0;
   cudaStream_t copy_ = nullptr;
+  cudaStream_t narrow_ = nullptr;  // high-priority stream of the GPU narrowing kernels
   unsigned long long* err_ = nullptr;
   double* loss_ = nullptr;
   double* h_loss_ = nullptr;  // pinned: a pageable D2H would block every other thread's CUDA calls
@@ -144,6 +153,7 @@ class EmbContext {
   int64_t n_units_ = 0;
   int64_t n_tma_units_ = 0;
   PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
+  int raw_eighths_ = 0;  // ASB_RAW_EIGHTHS: eighths of the index pieces narrowed on the GPU
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
   double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
   double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)

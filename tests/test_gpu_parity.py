@@ -496,3 +496,39 @@ def test_fp16_weight_storage(P, oracle, cuda, dims):
             assert np.array_equal(w, w.astype(np.float16).astype(np.float64))  # stored values are fp16
             ok, worst = fp_close(sh.read_momentum(t, r["rows"]), r["m"])
             assert ok, f"table {tab.id}: momentum off by {worst:.3g}x tolerance"
+
+
+def test_gpu_side_narrowing_and_validation(P, oracle, cuda, monkeypatch):
+    """ASB_RAW_EIGHTHS=8: every index piece of a pinned batch goes host->device
+    as int64 and is narrowed + validated on the GPU (narrow_validate_kernel).
+    Same device rows, bit-exact forward, and the same first error (table,
+    check, entry order; load_workload's message) as the host path."""
+    monkeypatch.setenv("ASB_RAW_EIGHTHS", "8")
+    pool = P.generate_pool(6, 5, P.GeneratorConfig(dim_choices=(16, 64), hash_size_max=3e4))
+    B, seed = 256, 2
+    wl = P.generate_workload(4, pool, B).pin()
+    st = streams_of(wl, pool)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(wl)
+        sh.forward()
+        assert np.array_equal(sh.read_pooled().astype(np.float64),
+                              oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed))
+        row0 = np.cumsum([0] + [t.hash_size for t in pool])[:-1]
+        glob = np.concatenate([idx + r0 for (_, idx), r0 in zip(st, row0)])
+        assert np.array_equal(sh.read_buffer(P.device.GLOBAL_ROWS), glob)
+        t3, t4 = pool[3], pool[4]
+        idx3, idx4 = wl.find(t3.id).indices, wl.find(t4.id).indices
+        keep = (idx3[2], idx3[5], idx4[1])
+        idx3[5], idx3[2], idx4[1] = t3.hash_size + 7, -3, t4.hash_size
+        sh.stage(wl)
+        with pytest.raises(P.IndexError_, match=rf"table {t3.id}: index -3 out of range \[0, {t3.hash_size}\)"):
+            sh.commit()
+        idx3[2] = keep[0]
+        sh.stage(wl)
+        with pytest.raises(P.IndexError_, match=rf"table {t3.id}: index {t3.hash_size + 7} out of range"):
+            sh.commit()
+        idx3[5], idx4[1] = keep[1], keep[2]
+        sh.load(wl)
+        sh.forward()
+        assert np.array_equal(sh.read_pooled().astype(np.float64),
+                              oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed))
