@@ -51,7 +51,8 @@ def main():
         plans[f"random-{s}"] = P.random_shard(task, s)
     for tag, fname in (("autoshard-rl", f"{args.workload}_autoshard_rl"),
                        ("autoshard-rl", f"{args.workload}_k{K}_autoshard_rl"),
-                       ("autoshard-rl-gpu", f"{args.workload}_autoshard_rl_gpu")):
+                       ("autoshard-rl-gpu", f"{args.workload}_autoshard_rl_gpu"),
+                       ("autoshard-rl-gpu-1200", f"{args.workload}_autoshard_rl_gpu2")):
         rl = os.path.join(ROOT, "plans", fname + ".assignment")
         if os.path.exists(rl):
             a = [int(x) for x in open(rl).read().split()]
