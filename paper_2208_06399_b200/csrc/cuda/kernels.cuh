@@ -458,8 +458,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
-#pragma unroll
           if constexpr (PAIR) {
+#pragma unroll
             for (int w = 0; w < NV; w += 2)
               gather8h(v[u][w], v[u][w + 1], EXACT || colv<GL, true>(c, w) < nvec, row + (w >> 1) * GL * 16);
           } else {
@@ -474,8 +474,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
         for (int u = 0; u < U; ++u) {
           const bool ok = m0 + u < nval;
           const char* row = row_addr(gbase, ASB_ROWID(ids[u]), gstride);
-#pragma unroll
           if constexpr (PAIR) {
+#pragma unroll
             for (int w = 0; w < NV; w += 2)
               gather8h(v[u][w], v[u][w + 1], ok && (EXACT || colv<GL, true>(c, w) < nvec), row + (w >> 1) * GL * 16);
           } else {
