@@ -421,6 +421,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
   for (int w = 0; w < NV; ++w) acc[w] = make_float4(0.f, 0.f, 0.f, 0.f);
   float loss_acc = 0.f;
+  bool hpend = false;  // this chunk ended a segment that began earlier (head carry stored)
 
   if (live)
     stage(j_lo, 0);
@@ -499,7 +500,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             const bool split = s == prev_seg;
             if (endu && split) {
               store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
-              if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
+              hpend = true;  // finished at the chunk end (inline or via the fixup list)
             }
             if constexpr (FWD) {
               if (endu && !split) store_pooled<GL, NV, PAIR>(p, tb, s, acc, c, loss_acc);
@@ -572,10 +573,45 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     __syncwarp();
   }
   cp_async_wait<0>();
-  // The chunk's last segment continues into the next chunk: hand the partial on.
+  // The chunk's last segment continues into the next chunk: hand the partial on
+  // (tail: the segment started in this chunk; through: the whole chunk is
+  // inside one segment).
+  int ckind = 0;  // 1: tail, 2: through
   if (live && j_hi < t_hi) {
     const int sl = __ldg(p.seg + j_hi - 1);
-    if (__ldg(p.seg + j_hi) == sl) store_carry<GL, NV, PAIR>(p, chunk, sl == prev_seg ? 0 : 1, nvec, c, acc);
+    if (__ldg(p.seg + j_hi) == sl) {
+      store_carry<GL, NV, PAIR>(p, chunk, sl == prev_seg ? 0 : 1, nvec, c, acc);
+      ckind = sl == prev_seg ? 2 : 1;
+    }
+  }
+  (void)ckind;
+  if constexpr (GL < 32) {
+    // A segment that began in the previous chunk and ended in this one, when
+    // that chunk is the previous group of THIS warp and left a tail: finish it
+    // here (tail[k-1] + head[k], the fixup's order; the warp barrier orders
+    // the other group's carry stores) instead of queueing it for the fixups.
+    __syncwarp();
+    const int pred_kind = __shfl_sync(0xffffffffu, ckind, (lane - GL) & 31);
+    const bool ready = hpend && g > 0 && pred_kind == 1;
+    if (__any_sync(0xffffffffu, ready)) {
+      float4 hv[NV];
+      const float* tail = p.carry + ((long long)(chunk - 1) * 2 + 1) * p.carry_stride;
+      const float* head = p.carry + ((long long)chunk * 2) * p.carry_stride;
+#pragma unroll
+      for (int w = 0; w < NV; ++w) {
+        const int cv = colv<GL, PAIR>(c, w);
+        hv[w] = (ready && cv < nvec) ? f4add(f4add(make_float4(0.f, 0.f, 0.f, 0.f),
+                                                   *reinterpret_cast<const float4*>(tail + cv * 4)),
+                                             *reinterpret_cast<const float4*>(head + cv * 4))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if constexpr (FWD) {
+        if (ready) store_pooled<GL, NV, PAIR>(p, tb, prev_seg, hv, c, loss_acc);
+      } else {
+        adagrad_row_pred<GL, NV>(p, tb, prev_seg, hv, c, ready);
+      }
+    }
+    if (hpend && !ready && c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
   }
   if constexpr (FWD) {
     if (p.loss) {
