@@ -437,7 +437,7 @@ def main():
     dom = max(phase_ms, key=phase_ms.get)
     dom_ms = phase_ms[dom] / K
     achieved = phase_bytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    traffic = ncu_traffic(dom, wname) if world == 1 and args.weights == "fp32" else None
+    traffic = (ncu_traffic(dom, wname) if world == 1 and args.weights == "fp32" and args.plan_shard < 0 else None)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "algorithmic_bytes_per_launch": phase_bytes[dom],
