@@ -29,10 +29,19 @@ namespace cubns = CUB_NS_QUALIFIER;
 
 constexpr int kHistThreads = 256;
 
+#ifndef ASB_SORT_PARTS
+#define ASB_SORT_PARTS 1
+#endif
+#ifndef ASB_SORT_RANK
+#define ASB_SORT_RANK RADIX_RANK_MATCH_EARLY_COUNTS_ANY
+#endif
+#ifndef ASB_SORT_SCAN
+#define ASB_SORT_SCAN BLOCK_SCAN_RAKING_MEMOIZE
+#endif
 using OnesweepPolicy =
-    cubns::AgentRadixSortOnesweepPolicy<ASB_SORT_THREADS, ASB_SORT_ITEMS, unsigned, 1,
-                                        cubns::RADIX_RANK_MATCH_EARLY_COUNTS_ANY, cubns::BLOCK_SCAN_RAKING_MEMOIZE,
-                                        cubns::RADIX_SORT_STORE_DIRECT, kSortBits>;
+    cubns::AgentRadixSortOnesweepPolicy<ASB_SORT_THREADS, ASB_SORT_ITEMS, unsigned, ASB_SORT_PARTS,
+                                        cubns::ASB_SORT_RANK, cubns::ASB_SORT_SCAN, cubns::RADIX_SORT_STORE_DIRECT,
+                                        kSortBits>;
 using OnesweepAgent = cubns::detail::radix_sort::AgentRadixSortOnesweep<OnesweepPolicy, false, unsigned, int, int, int>;
 
 
