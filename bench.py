@@ -363,15 +363,28 @@ def main():
             exch = PooledExchange(lay, rank, device="cuda")
             exchange = exchange or "NCCL all_to_all_single both ways"
 
-    def step():
+    xev = []  # (fwd a, fwd b, bwd a, bwd b) exchange events of the profiling pass
+
+    def step(timed_exchange=False):
         if world > 1:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timed_exchange else None
             if isinstance(exch, FusedPooledExchange):
-                recv = exch.forward(stream=stream)
+                recv = exch.forward(stream=stream)  # exchange inside K1/K4 + barrier
             else:
                 shard.forward(pooled, stream=stream)
+                if ev:
+                    ev[0].record(stream)
                 recv = exch.forward(pooled)
+                if ev:
+                    ev[1].record(stream)
             # dense part out of scope: loss 1/2|pooled|^2 -> dL/dpooled = pooled (recv)
-            shard.backward(exch.backward(recv), LR, EPS, stream=stream)
+            if ev:
+                ev[2].record(stream)
+            g = exch.backward(recv)
+            if ev:
+                ev[3].record(stream)
+                xev.append(ev)
+            shard.backward(g, LR, EPS, stream=stream)
         else:
             shard.forward(pooled, stream=stream)
             shard.backward(pooled, LR, EPS, stream=stream)
@@ -420,8 +433,23 @@ def main():
     shard.profile(True, serialize=True)
     for i in range(K):
         flush_buf.fill_(float(i))
-        step()
+        step(timed_exchange=True)
     torch.cuda.synchronize()
+    exchange_stats = None
+    if world > 1 and xev:
+        # NCCL convention: busbw = (bytes one rank sends / t) * (G-1)/G; max t over ranks
+        bwd_ms = sum(e[2].elapsed_time(e[3]) for e in xev) / len(xev)
+        fwd_ms = (sum(e[0].elapsed_time(e[1]) for e in xev) / len(xev)
+                  if not isinstance(exch, FusedPooledExchange) else None)
+        tx = torch.tensor([bwd_ms, fwd_ms or 0.0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tx, op=dist.ReduceOp.MAX)
+        bwd_ms, fwd_max = float(tx[0]), float(tx[1])
+        nbytes = 4 * B * max(lay.shard_dims)  # the largest owner's pooled block
+        busbw = lambda ms: round(nbytes / (ms / 1e3) / 1e9 * (world - 1) / world, 1) if ms > 0 else None
+        exchange_stats = {"bwd_a2a_ms": round(bwd_ms, 4), "bwd_busbw_gbs": busbw(bwd_ms),
+                          "fwd_a2a_ms": round(fwd_max, 4) if fwd_ms is not None else "fused into K1/K4 (peer stores)",
+                          "fwd_busbw_gbs": busbw(fwd_max) if fwd_ms is not None else None,
+                          "bytes_per_rank_max": nbytes * (world - 1) // world}
     phase_ms, _ = shard.profile_read(reset=True)
     shard.profile(False)
     # shard time = this rank's own kernels (serialized phases, no exchange): the
@@ -522,6 +550,7 @@ def main():
             "step_roofline": {"bytes_fwd": fwd_b, "bytes_bwd": bwd_b, "achieved_gbs": round(step_gbs, 1),
                               "frac": round(step_gbs / peak, 4)},
             "phase_ms_per_step": {k: round(v / K, 4) for k, v in phase_ms.items()},
+            "exchange_timing": exchange_stats,
             "shard_ms_per_step": [round(x, 4) for x in shard_ms],
             "max_shard_ms": round(max(shard_ms), 4),
             "balance": round(min(shard_ms) / max(shard_ms), 4) if max(shard_ms) > 0 else 1.0,
