@@ -532,3 +532,46 @@ def test_gpu_side_narrowing_and_validation(P, oracle, cuda, monkeypatch):
         sh.forward()
         assert np.array_equal(sh.read_pooled().astype(np.float64),
                               oracle.forward_f64(to_oracle_tables(pool), B, st, wseed=seed))
+
+
+def test_cfg4_shard_full_size_properties(P, cuda):
+    """An 8-GPU-sized slice of BASELINE cfg 4 at full batch (every 8th table of
+    pool856: 107 tables, dims 16/32, B = 65,536): narrow lane layouts, the
+    table-segmented sort (1-3 passes per table), in-warp and fixup completion
+    of hot rows. Bit-exact: each sampled table's sorted (row, bag) order equals
+    numpy's stable argsort; the pooled column sums equal sum(count * W[row]);
+    the momentum of sampled rows equals |g_r|^2 / D."""
+    pool = P.generate_pool(0, 856)[::8]
+    B, seed = 65536, 0
+    wl = P.generate_workload(0, pool, B)
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(wl)
+        sh.forward()
+        pooled = sh.read_pooled()
+        sh.backward(None, LR, EPS)
+        srows = sh.read_buffer(P.device.SORTED_ROWS)
+        sbags = sh.read_buffer(P.device.SORTED_BAGS)
+        row0 = np.cumsum([0] + [t.hash_size for t in pool])[:-1]
+        start = np.cumsum([0] + [len(wl.find(t.id).indices) for t in pool])
+        rng = np.random.default_rng(1)
+        for t in rng.choice(len(pool), size=8, replace=False):
+            tab = pool[t]
+            s = wl.find(tab.id)
+            bags = bag_ids(s.offsets)
+            order = np.argsort(s.indices, kind="stable")
+            a, b = start[t], start[t + 1]
+            assert np.array_equal(srows[a:b], s.indices[order] + row0[t]), tab.id
+            assert np.array_equal(sbags[a:b], bags[order]), tab.id
+            rows, counts = np.unique(s.indices, return_counts=True)
+            W = weight_rows(seed, tab.id, rows, tab.dim).astype(np.float64)
+            got = pooled[:, sh.cols[t]:sh.cols[t] + tab.dim].astype(np.float64).sum(0)
+            assert np.allclose(got, (W * counts[:, None]).sum(0), rtol=1e-9, atol=1e-6), tab.id
+            inv = np.searchsorted(rows, s.indices[order])
+            bounds = np.searchsorted(inv, np.arange(len(rows) + 1))
+            pick = np.concatenate([np.argsort(-counts)[:5], rng.choice(len(rows), size=min(100, len(rows)), replace=False)])
+            G = pooled[:, sh.cols[t]:sh.cols[t] + tab.dim].astype(np.float64)
+            mom = sh.read_momentum(int(t), rows[pick])
+            for q, k in enumerate(pick):
+                g = G[bags[order[bounds[k]:bounds[k + 1]]]].sum(0)
+                want = (g @ g) / tab.dim
+                assert abs(mom[q] - want) <= 1e-5 * want + 1e-30, (tab.id, rows[k], counts[k])
