@@ -478,7 +478,11 @@ def main():
     # the loss of each step is read back (D2H) and the batch's validation checked ----
     e2e = None
     if not args.no_e2e and not args.profile_only:
-        h2d = sum(8 * (B + 1) + 8 * l for l in L) + 40 * len(mine)
+        # bytes the staging pipeline copies host->device per step: int32 rows
+        # and rebased int32 offsets (narrowed from the caller's int64 CSR on the
+        # host), the per-batch table descriptors (~96 B each) and work maps
+        info = shard.info()
+        h2d = 4 * sum(L) + 4 * (len(mine) * B + 1) + 96 * len(mine) + 4 * int(info.n_chunks)
         d2h = 8 + 8
 
         def e2e_step():
