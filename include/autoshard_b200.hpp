@@ -155,11 +155,12 @@ std::vector<double> measure_plan(const Plan& plan, const Task& task, const Workl
 // One shard resident on one device (RAII over as_ctx).
 class Shard {
  public:
+  // flags: 0 (fp32 tables) or AS_WEIGHTS_FP16 (bytes_per_param 2 storage)
   template <class Tables>
-  Shard(int device, const Tables& tables, int64_t batch, uint64_t weight_seed = 0) {
+  Shard(int device, const Tables& tables, int64_t batch, uint64_t weight_seed = 0, int32_t flags = 0) {
     const auto specs = to_specs(tables);
     as_ctx* c = nullptr;
-    check(as_create(device, specs.data(), static_cast<int32_t>(specs.size()), batch, weight_seed, &c));
+    check(as_create_ex(device, specs.data(), static_cast<int32_t>(specs.size()), batch, weight_seed, flags, &c));
     ctx_.reset(c);
   }
   template <class WorkloadT, class Tables>
@@ -168,6 +169,10 @@ class Shard {
     check(as_load_workload(ctx_.get(), v.get(), stream));
   }
   void forward(float* out = nullptr, void* stream = nullptr) { check(as_forward(ctx_.get(), out, stream)); }
+  // fused forward exchange: pooled row b -> peer_bases[b / rows_per_peer] (as_set_peer_outputs)
+  void set_peer_outputs(const std::vector<float*>& peer_bases, int64_t rows_per_peer) {
+    check(as_set_peer_outputs(ctx_.get(), static_cast<int>(peer_bases.size()), peer_bases.data(), rows_per_peer));
+  }
   void backward(const float* grad, float lr, float eps, void* stream = nullptr) {
     check(as_backward_rowwise_adagrad(ctx_.get(), grad, lr, eps, stream));
   }

@@ -12,6 +12,8 @@
 // writes <out_prefix>.assignment (one line, n_target shard ids) and
 // <out_prefix>.ckpt (the reference checkpoint, ASHCKPT1).
 //
+// RL_SEED=s: TrainConfig::seed (model init and actor streams), for seed studies.
+//
 // TRAIN_RANGE=a:b: train on subsets of pool tables [a, b) instead of
 // [n_target, n_pool) — BASELINE cfg 5 (856 tables, 50% unseen): n_pool =
 // n_target = 856, TRAIN_RANGE=0:428.
@@ -166,6 +168,7 @@ int main(int argc, char** argv) {
 
   rl::TrainConfig cfg;
   cfg.max_updates = max_updates;
+  if (const char* s = std::getenv("RL_SEED")) cfg.seed = std::strtoull(s, nullptr, 10);  // TrainConfig::seed
   cfg.max_seconds = max_seconds;
   cfg.eval_every = 10;
   const auto t0 = std::chrono::steady_clock::now();
