@@ -73,6 +73,13 @@ def main():
                 load[k] += ms[str(tables[i].id)]
                 used[k] += tables[i].size_bytes()
             plans["measured-greedy"] = P.ShardingPlan(a)
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "plans", f"{args.workload}_autoshard_rl_s*.assignment"))):
+        tag = "autoshard-rl-" + os.path.basename(path).split("_autoshard_rl_")[1].split(".")[0]  # seed runs
+        a = [int(x) for x in open(path).read().split()]
+        if len(a) == len(tables) and max(a) < K:
+            plans[tag] = P.ShardingPlan(a)
     if args.plans:
         keep = set(args.plans.split(","))
         plans = {k: v for k, v in plans.items() if k in keep or k.split("-")[0] in keep}
