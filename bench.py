@@ -66,6 +66,18 @@ def build_workload(P, name):
     raise SystemExit(f"unknown workload {name}")
 
 
+def same_workload_n1(wname):
+    """N>1 runs use BASELINE cfg 4 while N=1 reports cfg 2 (the metric's
+    single-GPU config): the committed N=1 line of THIS workload, so scaling can
+    be read on one workload."""
+    path = os.path.join(ROOT, "profiles", f"r1_bench_{wname}.json")
+    try:
+        d = json.load(open(path))
+        return {"value": d["value"], "ms_per_step": d["ms_per_step"], "source": os.path.relpath(path, ROOT)}
+    except Exception:
+        return None
+
+
 def bench_plan(P, task, wname, world):
     """The sharding plan of an N>1 run: the AutoShard-RL plan produced by the
     reference trainer for this config and shard count (plans/<cfg>_k<N>_autoshard_rl.assignment,
@@ -555,6 +567,7 @@ def main():
                               "frac": round(step_gbs / peak, 4)},
             "phase_ms_per_step": {k: round(v / K, 4) for k, v in phase_ms.items()},
             "exchange_timing": exchange_stats,
+            "same_workload_n1": same_workload_n1(wname) if world > 1 else None,
             "shard_ms_per_step": [round(x, 4) for x in shard_ms],
             "max_shard_ms": round(max(shard_ms), 4),
             "balance": round(min(shard_ms) / max(shard_ms), 4) if max(shard_ms) > 0 else 1.0,
