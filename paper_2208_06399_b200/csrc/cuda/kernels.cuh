@@ -354,7 +354,10 @@ __host__ __device__ constexpr int stage_s_ints(int kind) { return (32 / kind_gl(
 #endif
 template <bool FWD, int GL, int NV, bool EXACT, bool HALF, bool PAIR_>
 __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb, int t, int unit, int* xs, int* ss) {
-  const int kStageX = p.stage_x, kStageS = p.stage_s;
+  // this layout's buffer sizes (compile-time; the warp's smem region is sized
+  // by the host for the shard's widest layout, so these always fit)
+  constexpr int kStageX = (32 / GL) * ((8 * GL < 32) ? 8 * GL : 32);
+  constexpr int kStageS = (32 / GL) * (((8 * GL < 32) ? 8 * GL : 32) + 1);
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
   constexpr int Q = SR / GL;                       // elements staged per lane per super-round
