@@ -75,8 +75,9 @@ def main():
             plans["measured-greedy"] = P.ShardingPlan(a)
     import glob
 
-    for path in sorted(glob.glob(os.path.join(ROOT, "plans", f"{args.workload}_autoshard_rl_s*.assignment"))):
-        tag = "autoshard-rl-" + os.path.basename(path).split("_autoshard_rl_")[1].split(".")[0]  # seed runs
+    for path in sorted(glob.glob(os.path.join(ROOT, "plans", f"{args.workload}_autoshard_rl_s*.assignment")) +
+                       glob.glob(os.path.join(ROOT, "plans", f"{args.workload}_k{K}_autoshard_rl_*.assignment"))):
+        tag = "autoshard-rl-" + os.path.basename(path).split("_autoshard_rl_")[1].split(".")[0]  # seed / longer runs
         a = [int(x) for x in open(path).read().split()]
         if len(a) == len(tables) and max(a) < K:
             plans[tag] = P.ShardingPlan(a)
