@@ -193,10 +193,10 @@ __device__ __forceinline__ int colv(int c, int w) {
 
 // Segment epilogues, executed by the GL lanes of one group.
 // forward : pooled[bag, col_t + :] = v   (+ loss 1/2|v|^2)
-template <int GL, int NV, bool PAIR = false>
+template <int GL, int NV, bool PAIR = false, bool EX = false>
 __device__ __forceinline__ void store_pooled(const SegParams& p, const DevTable& tb, int seg, const float4 (&v)[NV],
                                              int c, float& loss_acc) {
-  const int nvec = tb.dim >> 2;
+  const int nvec = EX ? GL * NV : tb.dim >> 2;
   float* o = pooled_row(p.out, p.out_stride, p.peers, seg) + tb.col;
 #pragma unroll
   for (int w = 0; w < NV; ++w) {
@@ -366,7 +366,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const int g = lane / GL;
   const int c = lane % GL;
   const unsigned gmask = low_bits<GL>() << (g * GL);
-  const int nvec = tb.dim >> 2;
+  // forward, EXACT layouts: the row width is a compile-time constant
+  const int nvec = (FWD && EXACT) ? GL * NV : (tb.dim >> 2);
   const int C = tb.chunk_len;
   const int lchunk = (unit - tb.unit_off) * R + g;
   const int chunk = tb.chunk_off + lchunk;
@@ -386,7 +387,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   if constexpr (FWD) {
     gbase = HALF ? reinterpret_cast<const char*>(reinterpret_cast<const __half*>(p.W_ro) + tb.w_base)
                  : reinterpret_cast<const char*>(p.W_ro + tb.w_base);
-    gstride = (unsigned)tb.dim * (HALF ? 2u : 4u);
+    gstride = EXACT ? (unsigned)(GL * NV * (HALF ? 8 : 16)) : (unsigned)tb.dim * (HALF ? 2u : 4u);
   } else {
     gbase = reinterpret_cast<const char*>(p.grad + tb.col);
     gstride = (unsigned)p.grad_stride * 4u;
@@ -506,7 +507,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
               hpend = true;  // finished at the chunk end (inline or via the fixup list)
             }
             if constexpr (FWD) {
-              if (endu && !split) store_pooled<GL, NV, PAIR>(p, tb, s, acc, c, loss_acc);
+              if (endu && !split) store_pooled<GL, NV, PAIR, EXACT>(p, tb, s, acc, c, loss_acc);
             } else {
               adagrad_row_pred<GL, NV>(p, tb, s, acc, c, endu && !split);
             }
@@ -549,7 +550,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
               store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
               if (c == 0) p.completers[atomicAdd(p.n_completers, 1)] = make_int2(chunk, t);
             } else if constexpr (FWD) {
-              store_pooled<GL, NV, PAIR>(p, tb, s, acc, c, loss_acc);
+              store_pooled<GL, NV, PAIR, EXACT>(p, tb, s, acc, c, loss_acc);
             } else {
 #ifdef ASB_ABLATE_EPILOGUE  // ablation builds only: write g, skip the row update
               if (c == 0) p.M[tb.row_off + s] = acc[0].x;
@@ -609,7 +610,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       if constexpr (FWD) {
-        if (ready) store_pooled<GL, NV, PAIR>(p, tb, prev_seg, hv, c, loss_acc);
+        if (ready) store_pooled<GL, NV, PAIR, EXACT>(p, tb, prev_seg, hv, c, loss_acc);
       } else {
         adagrad_row_pred<GL, NV>(p, tb, prev_seg, hv, c, ready);
       }
