@@ -103,10 +103,11 @@ def main():
         print(f"{name:14s} max {max(costs):7.3f} ms  balance {res[name]['balance']:.3f}  "
               f"shards {' '.join(f'{c:.3f}' for c in costs)}", flush=True)
     rnd = [res[k]["max_ms"] for k in res if k.startswith("random-")]
-    rnd_mean = sum(rnd) / len(rnd)
+    rnd_mean = sum(rnd) / len(rnd) if rnd else None
     for k, v in res.items():
-        v["speedup_vs_random_mean"] = rnd_mean / v["max_ms"]
-        v["speedup_vs_lookup_greedy"] = res["lookup-greedy"]["max_ms"] / v["max_ms"]
+        v["speedup_vs_random_mean"] = rnd_mean / v["max_ms"] if rnd_mean else None
+        v["speedup_vs_lookup_greedy"] = (res["lookup-greedy"]["max_ms"] / v["max_ms"]
+                                         if "lookup-greedy" in res else None)
     out = {"workload": args.workload, "desc": desc, "shards": K, "batch": B, "weights": args.weights,
            "budget_rule": "1.6 x total / K (SPEC.md:620), bytes_per_param 2",
            "protocol": f"W={args.warmup} B={args.measure} R={args.trim}, L2 flushed, one shard at a time on 1 GPU",
@@ -115,8 +116,8 @@ def main():
         with open(args.out, "w") as f:
             json.dump(out, f, indent=1)
     print(json.dumps({k: {"max_ms": round(v["max_ms"], 3), "balance": round(v["balance"], 3),
-                          "speedup_vs_random": round(v["speedup_vs_random_mean"], 3),
-                          "speedup_vs_lookup_greedy": round(v["speedup_vs_lookup_greedy"], 3)}
+                          "speedup_vs_random": v["speedup_vs_random_mean"] and round(v["speedup_vs_random_mean"], 3),
+                          "speedup_vs_lookup_greedy": v["speedup_vs_lookup_greedy"] and round(v["speedup_vs_lookup_greedy"], 3)}
                       for k, v in res.items()}))
 
 
