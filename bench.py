@@ -66,32 +66,36 @@ def build_workload(P, name):
     raise SystemExit(f"unknown workload {name}")
 
 
-def same_workload_n1(wname):
-    """N>1 runs use BASELINE cfg 4 while N=1 reports cfg 2 (the metric's
-    single-GPU config): the committed N=1 line of THIS workload, so scaling can
-    be read on one workload."""
-    path = os.path.join(ROOT, "profiles", f"r1_bench_{wname}.json")
-    try:
-        d = json.load(open(path))
-        return {"value": d["value"], "ms_per_step": d["ms_per_step"], "source": os.path.relpath(path, ROOT)}
-    except Exception:
-        return None
+def device_task(P, tables, K, weights="fp32"):
+    """The ShardingTask the bench places tables with: bytes_per_param = the
+    device's storage bytes (4 fp32 / 2 fp16, tables.hpp:30), per-GPU budget =
+    HBM left for the tables after momentum, pooled buffers and workspaces."""
+    import copy
+
+    tabs = [copy.copy(t) for t in tables]
+    for t in tabs:
+        t.bytes_per_param = 4 if weights == "fp32" else 2
+    return P.ShardingTask(tabs, K, [PLAN_BUDGET_BYTES] * K)
+
+
+PLAN_BUDGET_BYTES = 160_000_000_000  # of the B200's 180 GB: tables; the rest is momentum, pooled rows, scratch
 
 
 def bench_plan(P, task, wname, world):
-    """The sharding plan of an N>1 run: the AutoShard-RL plan produced by the
-    reference trainer for this config and shard count (plans/<cfg>_k<N>_autoshard_rl.assignment,
-    oracle/rl_plans.cpp; BASELINE cfg 4 names the AutoShard-RL plan), else
-    lookup-greedy (planners.hpp:73-107)."""
-    for name in (f"{wname}_k{world}_autoshard_rl.assignment", f"{wname}_autoshard_rl.assignment"):
-        path = os.path.join(ROOT, "plans", name)
-        if os.path.exists(path):
-            a = [int(x) for x in open(path).read().split()]
-            if len(a) == len(task.tables) and max(a) < world:
-                plan = P.ShardingPlan(a)
-                if plan.feasible(task):
-                    return plan, f"autoshard-rl (plans/{name}, reference trainer)"
-    return P.greedy_shard(task, P.HeuristicKind.kLookupGreedy), "lookup-greedy (planners.hpp:73-107)"
+    """The sharding plan of an N>1 run: the AutoShard-RL plan of the reference
+    trainer for this config and shard count, stored as a fingerprinted plan
+    file (plans/<cfg>_k<N>_autoshard_rl.plan, "autoshard-plan 1" format,
+    loaded with as_plan_load which rejects a plan made for another task);
+    else lookup-greedy (planners.hpp:73-107). Either must be feasible for the
+    device task (fp32 bytes per parameter)."""
+    path = os.path.join(ROOT, "plans", f"{wname}_k{world}_autoshard_rl.plan")
+    if os.path.exists(path):
+        plan, _ = P.load_plan(path, task)
+        if not plan.feasible(task):
+            raise SystemExit(f"{path}: plan does not fit the per-GPU budget")
+        return plan, f"autoshard-rl ({os.path.relpath(path, ROOT)}, reference trainer, fingerprint checked)"
+    plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
+    return plan, "lookup-greedy (planners.hpp:73-107)"
 
 
 def nominal_bytes(tables, B, L, U, wb=4):
@@ -184,100 +188,97 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def common_config(wname, n_tables, B):
+    """The `config` both arms print (identical by construction)."""
+    return {"workload": wname, "tables": n_tables, "global_batch": B,
+            "l2": "GPU arm: L2 flushed (2x L2 fill) between timed steps, flush not timed; "
+                  "CPU arm: dense tables (>= 33 GB) far larger than the host caches"}
+
+
 def measured_peak_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 7700.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel, workload):
-    """dram bytes/launch of `kernel` from the committed ncu --set full summary, if it matches."""
+def sources_sha():
+    """Identity of the native build: sha256 over the library's CUDA/C++ sources
+    and the C-ABI header. An ncu summary carries the sha of the sources it was
+    captured on; bench.py uses its DRAM bytes only when they match."""
+    import hashlib
+
+    h = hashlib.sha256()
+    base = os.path.join(ROOT, "paper_2208_06399_b200", "csrc")
+    files = []
+    for dp, dn, fs in os.walk(base):
+        dn[:] = sorted(d for d in dn if d != "build")
+        files += [os.path.join(dp, f) for f in fs if f.endswith((".cu", ".cuh", ".hpp", ".cpp", ".h")) or f == "Makefile"]
+    files.append(os.path.join(ROOT, "include", "autoshard_b200.h"))
+    for path in sorted(files):
+        h.update(os.path.relpath(path, ROOT).encode())
+        with open(path, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(kernel, workload, sha):
+    """DRAM bytes (read + write) per launch of `kernel` from profiles/ncu_traffic.json
+    (tools/ncu_summary.py over an `ncu --set full` capture) when the capture was
+    taken on these sources; else (None, why)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)
-        e = d.get(workload, {}).get(kernel)
-        return float(e["dram_bytes_per_launch"]) if e else None
+            d = json.load(f).get(workload)
     except Exception:
-        return None
+        return None, "no profiles/ncu_traffic.json"
+    if not d or "kernels" not in d:
+        return None, f"no ncu capture of {workload}"
+    if d.get("sources_sha") != sha:
+        return None, f"ncu capture of {workload} is from other sources ({d.get('sources_sha')} != {sha})"
+    e = d["kernels"].get(kernel)
+    if not e:
+        return None, f"ncu capture of {workload} has no {kernel}"
+    return float(e["dram_bytes_per_launch"]), f"profiles/{e['summary']} (sources {sha})"
+
+
+def compulsory_bytes(tables, B, L, U, passes, wb=4):
+    """Per-phase MINIMUM DRAM traffic: every distinct weight row, gradient row
+    and index read or written once (the §8d nominal model counts every gather)."""
+    s = 4
+    T = len(tables)
+    SD = sum(t.dim for t in tables)
+    UD = sum(u * t.dim for u, t in zip(U, tables))
+    Lt, Ut = sum(L), sum(U)
+    return {
+        "bag_expand": s * (T * (B + 1) + Lt),
+        "fwd_segreduce": s * (2 * Lt + B * SD) + wb * UD,
+        "fwd_fixup": 0,
+        "radix_sort": s * Lt + sum(16 * l * p for l, p in zip(L, passes)),
+        "bwd_segreduce_adagrad": s * (2 * Lt + B * SD) + 2 * wb * UD + 2 * s * Ut,
+        "bwd_fixup": 0,
+    }
+
+
+def sort_passes(tables):
+    return [max(1, (max(1, (t.hash_size - 1).bit_length()) + 7) // 8) for t in tables]
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port; test infrastructure, only ever the checker/baseline)
+# CPU baseline (oracle/cpu_baseline.py: test infrastructure, the baseline only)
 # ---------------------------------------------------------------------------
-class CpuSample:
-    """oracle/orc_cpu_step_f32 (the CPU port of the path) on a prefix of the
-    tables whose dense fp32 weights fit max_weight_bytes; times scale to the
-    full workload by gathered bytes (sum L_t * dim_t)."""
+def cpu_baseline_leg(tables, wl, B, warmup=1, steps=3):
+    """GPU arm's cpu_baseline: the CPU port on ALL of this run's tables and the
+    same streams (bounded by steps, not by sampling tables)."""
+    from oracle.cpu_baseline import CpuBaseline, cpu_host
 
-    def __init__(self, tables, wl, B, max_weight_bytes=3 << 30, threads=0):
-        from oracle import Oracle
-
-        self.o = o = Oracle()
-        sub, wb = [], 0
-        for t in tables:
-            b = t.hash_size * t.dim * 4
-            if sub and wb + b > max_weight_bytes:
-                continue
-            sub.append(t)
-            wb += b
-            if wb > max_weight_bytes * 0.9:
-                break
-        self.W = np.empty(sum(t.hash_size * t.dim for t in sub), dtype=np.float32)
-        off = 0
-        for t in sub:
-            o.fill_weights(WEIGHT_SEED, t, self.W[off:off + t.hash_size * t.dim].reshape(t.hash_size, t.dim))
-            off += t.hash_size * t.dim
-        self.M = np.zeros(sum(t.hash_size for t in sub), dtype=np.float32)
-        self.out = np.empty((B, sum(t.dim for t in sub)), dtype=np.float32)
-        self.streams = [(wl.find(t.id).offsets, wl.find(t.id).indices) for t in sub]
-        self.dims = [t.dim for t in sub]
-        self.hashes = [t.hash_size for t in sub]
-        self.sub, self.tables, self.B, self.threads = sub, tables, B, threads
-        ld_full = sum(len(wl.find(t.id).indices) * t.dim for t in tables)
-        ld_sub = sum(len(s[1]) * t.dim for s, t in zip(self.streams, sub))
-        self.scale = ld_full / max(1, ld_sub)
-        self.cores = 1
-
-    def step(self):
-        t0 = time.perf_counter()
-        self.cores = self.o.cpu_step_f32(self.dims, self.hashes, self.B, self.streams, self.W, self.M, self.out,
-                                         LR, EPS, self.threads)
-        return time.perf_counter() - t0
-
-    def result(self, t_sample, n):
-        sub = self.sub
-        return {
-            "value": round(self.B / (t_sample * self.scale), 2),
-            "unit": "samples/s",
-            "cores": self.cores,
-            "kind": "port",
-            "sample": (f"oracle/orc_cpu_step_f32 (fp32 fwd + radix-sort bwd + row-wise Adagrad, OpenMP) on "
-                       f"{len(sub)}/{len(self.tables)} tables (ids {sub[0].id}..{sub[-1].id}), full batch {self.B}; "
-                       f"median of {n} steps = {t_sample * 1e3:.1f} ms, scaled x{self.scale:.2f} by gathered bytes"),
-            "host": cpu_host(),
-        }
-
-
-def cpu_sample(tables, wl, B, steps=3):
-    cs = CpuSample(tables, wl, B)
-    cs.step()  # warm-up
-    t = statistics.median([cs.step() for _ in range(steps)])
-    return cs.result(t, steps)
-
-
-def cpu_host():
-    model = ""
-    try:
-        with open("/proc/cpuinfo") as f:
-            for ln in f:
-                if ln.startswith("model name"):
-                    model = ln.split(":", 1)[1].strip()
-                    break
-    except OSError:
-        pass
-    return {"nproc": os.cpu_count(), "model": model}
+    streams = {t.id: (wl.find(t.id).offsets, wl.find(t.id).indices) for t in tables}
+    cb = CpuBaseline(tables, streams, B)
+    mean, ts, r = cb.run(warmup, steps, trim=0)
+    med = statistics.median(ts)
+    return {"value": round(B / med, 2), "unit": "samples/s", "cores": cb.cores, "kind": "port",
+            "sample": f"{cb.describe()}; {warmup} warm-up + median of {steps} steps = {med * 1e3:.1f} ms/step",
+            "host": cpu_host()}
 
 
 # ---------------------------------------------------------------------------
@@ -330,14 +331,13 @@ def main():
     if world > 1:
         if B % world:
             raise SystemExit("batch must divide by the GPU count")
-        budget = [int(180e9)] * world
-        task = P.ShardingTask(tables_all, world, budget)
+        task = device_task(P, tables_all, world, args.weights)
         plan, plan_name = bench_plan(P, task, wname, world)
         mine = [t for t, k in zip(tables_all, plan.assignment) if k == rank]
     elif args.plan_shard >= 0:
         # one shard of the K-GPU plan on this GPU (the per-GPU work of the K-GPU
         # run; the K-GPU box time is the max over its shards)
-        task = P.ShardingTask(tables_all, args.plan_k, [int(180e9)] * args.plan_k)
+        task = device_task(P, tables_all, args.plan_k, args.weights)
         plan, plan_name = bench_plan(P, task, wname, args.plan_k)
         plan_name = f"shard {args.plan_shard} of {args.plan_k}: {plan_name}"
         mine = [t for t, k in zip(tables_all, plan.assignment) if k == args.plan_shard]
@@ -476,12 +476,38 @@ def main():
     peak, peak_kind = measured_peak_hbm()
     dom = max(phase_ms, key=phase_ms.get)
     dom_ms = phase_ms[dom] / K
-    achieved = phase_bytes[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    traffic = (ncu_traffic(dom, wname) if world == 1 and args.weights == "fp32" and args.plan_shard < 0 else None)
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "algorithmic_bytes_per_launch": phase_bytes[dom],
-                "ms_per_launch": round(dom_ms, 4)}
+    wbytes = 2 if args.weights == "fp16" else 4
+    comp = compulsory_bytes(mine, B, L, U, sort_passes(mine), wb=wbytes)
+    prof_key = wname if (world == 1 and args.plan_shard < 0) else f"{wname}_k{world if world > 1 else args.plan_k}s{rank if world > 1 else args.plan_shard}"
+    if args.weights != "fp32":
+        prof_key += "_fp16"
+    traffic, traffic_src = ncu_traffic(dom, prof_key, sources_sha())
+    gbs = lambda nbytes: nbytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    # roofline: HBM bytes the kernel actually moved (ncu DRAM read+write of this
+    # build) over its live launch time; with no matching capture, its
+    # compulsory bytes (a lower bound of the DRAM traffic). The §8d nominal
+    # bytes count every gathered row and mostly hit L1/L2 at Zipf access:
+    # reported against the MEASURED L2 random-gather ceiling instead.
+    row_bytes = min(512, max(16, 1 << (max(t.dim for t in mine) * wbytes - 1).bit_length())) if mine else 512
+    try:
+        l2_peak = P.probe_gather_bw(min(64 << 20, int(l2 // 2)), row_bytes, device=local)
+        hbm_gather = P.probe_gather_bw(8 << 30, row_bytes, device=local)
+    except Exception:  # noqa: BLE001
+        l2_peak = hbm_gather = None
+    hbm_bytes = traffic if traffic is not None else comp[dom]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(gbs(hbm_bytes), 1), "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs(hbm_bytes) / peak, 4),
+                "traffic": traffic,
+                "achieved_basis": ("ncu DRAM bytes per launch, " + traffic_src) if traffic is not None else
+                                  f"compulsory bytes per launch ({traffic_src})",
+                "ms_per_launch": round(dom_ms, 4),
+                "compulsory_bytes_per_launch": comp[dom],
+                "algorithmic_bytes_per_launch": phase_bytes[dom],
+                "nominal_gbs": round(gbs(phase_bytes[dom]), 1),
+                "l2_gather_peak_gbs": round(l2_peak, 1) if l2_peak else None,
+                "hbm_gather_peak_gbs": round(hbm_gather, 1) if hbm_gather else None,
+                "gather_row_bytes": row_bytes,
+                "l2_frac": round(gbs(phase_bytes[dom]) / l2_peak, 4) if l2_peak else None}
     step_gbs = (fwd_b + bwd_b) / (ms_per_step / 1e3) / 1e9
 
     # ---- e2e through the public API: every step's int64 streams go host (pinned)
@@ -529,7 +555,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_only:
-        cpu = cpu_sample(mine, wl, B)
+        cpu = cpu_baseline_leg(mine, wl, B)
 
     if rank == 0:
         line = {
@@ -545,11 +571,9 @@ def main():
             "vs_baseline": None,
             "dtype": "fp32" if args.weights == "fp32" else "fp32 (fp16 table storage)",
             "data": "synthetic (reference generator, bit-exact; weights: counter-hash grid init)",
-            "config": {
-                "workload": wname,
+            "config": common_config(wname, len(tables_all), B),
+            "setup": {
                 "desc": wdesc,
-                "tables": len(tables_all),
-                "global_batch": B,
                 "sum_dim": sum(t.dim for t in tables_all),
                 "lookups": int(sum(L)) if world == 1 else None,
                 "plan": plan_name,
@@ -558,16 +582,15 @@ def main():
                 "exchange": exchange,
                 "step": "K4 bag-expand + fwd segreduce + fixup + radix sort + bwd segreduce/row-wise Adagrad + fixup"
                         + (" + pooled-row exchange both ways" if world > 1 else "") + "; grad = pooled (loss 1/2|pooled|^2)",
-                "l2": "flushed (2x L2 fill) between timed steps, flush excluded from step time",
                 "lr": LR,
                 "eps": EPS,
+                "sources_sha": sources_sha(),
             },
             "roofline": roofline,
             "step_roofline": {"bytes_fwd": fwd_b, "bytes_bwd": bwd_b, "achieved_gbs": round(step_gbs, 1),
                               "frac": round(step_gbs / peak, 4)},
             "phase_ms_per_step": {k: round(v / K, 4) for k, v in phase_ms.items()},
             "exchange_timing": exchange_stats,
-            "same_workload_n1": same_workload_n1(wname) if world > 1 else None,
             "shard_ms_per_step": [round(x, 4) for x in shard_ms],
             "max_shard_ms": round(max(shard_ms), 4),
             "balance": round(min(shard_ms) / max(shard_ms), 4) if max(shard_ms) > 0 else 1.0,
@@ -585,56 +608,51 @@ def main():
         dist.destroy_process_group()
 
 
-def reference_pieces(P, tables, B, wl):
-    """the reference's own CPU pieces on the path, timed single-threaded
-    as the reference runs them (oracle/_ref/libref.so = the unmodified headers compiled
-    in place), next to this repo's host equivalents on the same inputs."""
+def reference_pieces(tables, B, streams_src):
+    """the reference's own CPU pieces on the path, single-threaded
+    as the reference runs them (oracle/_ref/libref.so = the unmodified headers
+    compiled in place)."""
     try:
-        from oracle import Ref, Table
-    except Exception as e:  # noqa: BLE001
-        return {"unavailable": f"{type(e).__name__}: {e}"}
-    try:
+        from oracle import Ref
         ref = Ref()
     except Exception as e:  # noqa: BLE001
-        return {"unavailable": str(e)}
-    otabs = [Table(t.id, t.dim, t.hash_size, t.pooling_mean, t.access_ratio, t.bytes_per_param) for t in tables]
-    budgets = [sum(t.size_bytes() for t in tables)]
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    budgets = [sum(t.dim * t.hash_size * t.bytes_per_param for t in tables)]
     out = {"threads": 1, "tables": len(tables), "batch": B}
     t0 = time.perf_counter()
-    h, _ = ref.generate_workload(0, otabs, B)
+    h, _ = ref.generate_workload(0, tables, B)
     out["generate_workload_s"] = round(time.perf_counter() - t0, 3)
     t0 = time.perf_counter()
-    ref.measure_plan(otabs, budgets, [0] * len(otabs), h)
+    ref.measure_plan(tables, budgets, [0] * len(tables), h)
     out["measure_plan_sim_s"] = round(time.perf_counter() - t0, 3)
     t0 = time.perf_counter()
     for k in (0, 1, 2):
-        ref.greedy_shard(otabs, budgets, k)
+        ref.greedy_shard(tables, budgets, k)
     out["greedy_x3_s"] = round(time.perf_counter() - t0, 6)
     ref.free_workload(h)
-    t0 = time.perf_counter()
-    P.generate_workload(0, tables, B)
-    out["ours_generate_workload_s"] = round(time.perf_counter() - t0, 3)
-    out["ours_generate_workload_threads"] = os.cpu_count()
     return out
 
 
 def run_reference(args, world, rank, wname):
-    """CPU arm: the reference has no embedding arithmetic, so the
-    reference-side implementation of the path is the oracle port (fp32, OpenMP,
-    all host threads), timed on a bounded sample of the same workload."""
+    """Reference arm: the reference has no embedding arithmetic,
+    so the CPU implementation of the path is the oracle port, stepped over
+    EVERY table of the workload on all host threads, with the W/B/R protocol
+    (simcost.hpp:140-154). Tables and streams come from the reference's own
+    generator (oracle/_ref); nothing of paper_2208_06399_b200 is imported."""
     if rank != 0:
         return
-    import paper_2208_06399_b200 as P  # host generator only (no device calls)
+    from oracle.cpu_baseline import CpuBaseline, cpu_host, generate_streams, workload_tables
 
-    tables, B, wdesc = build_workload(P, wname)
-    wl = P.generate_workload(0, tables, B)
-    pieces = reference_pieces(P, tables, B, wl) if os.environ.get("ASB_REF_PIECES", "1") != "0" else None
-    cs = CpuSample(tables, wl, B)
-    for _ in range(args.warmup):
-        cs.step()
-    ts = [cs.step() for _ in range(args.steps)]
-    cpu = cs.result(statistics.median(ts), len(ts))
-    v = cpu["value"]
+    tables, B, zipf, tsrc = workload_tables(wname)
+    t0 = time.perf_counter()
+    streams, ssrc = generate_streams(tables, B, zipf)
+    gen_s = time.perf_counter() - t0
+    pieces = (reference_pieces(tables, B, ssrc) if wname in ("cfg1", "cfg2") and os.environ.get("ASB_REF_PIECES", "1") != "0"
+              else None)
+    cb = CpuBaseline(tables, streams, B)
+    trim = min(2, (args.steps - 1) // 2)
+    mean, ts, r = cb.run(args.warmup, args.steps, trim=trim)
+    v = B / mean
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -643,14 +661,19 @@ def run_reference(args, world, rank, wname):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(B / v * 1e3, 3),
+        "ms_per_step": round(mean * 1e3, 3),
         "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None,
         "dtype": "fp32",
-        "data": "synthetic (reference generator, bit-exact)",
-        "config": {"workload": wname, "desc": wdesc, "tables": len(tables), "global_batch": B},
-        "cpu_baseline": cpu,
+        "data": f"synthetic (tables: {tsrc}; streams: {ssrc})",
+        "config": common_config(wname, len(tables), B),
+        "cpu_baseline": {"value": round(v, 2), "unit": "samples/s", "cores": cb.cores, "kind": "port",
+                         "sample": f"{cb.describe()}; W={args.warmup}, B={args.steps}, R={r}: trimmed mean "
+                                   f"{mean * 1e3:.1f} ms/step (min {ts[0] * 1e3:.1f}, max {ts[-1] * 1e3:.1f})",
+                         "host": cpu_host()},
+        "step_s_sorted": [round(x, 4) for x in ts],
+        "generate_s": round(gen_s, 2),
         "reference_pieces": pieces,
         "e2e": {"value": round(v, 2), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

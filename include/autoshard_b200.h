@@ -289,6 +289,12 @@ AS_API as_status as_profile_read(as_ctx* ctx, double* ms_per_phase, int64_t* lau
  * table's distinct rows. Synchronises. */
 AS_API as_status as_table_features(as_ctx* ctx, double* out, void* stream);
 
+/* Roofline denominator (bench.py): GB/s of random row gathers of row_bytes
+ * (16..512, power of two) over a device buffer of footprint_bytes — an
+ * L2-resident footprint measures the L2 gather ceiling of cache-resident
+ * workloads, a multi-GB one the HBM gather ceiling. Synchronises. */
+AS_API as_status as_probe_gather_bw(int32_t device, int64_t footprint_bytes, int32_t row_bytes, double* gbs);
+
 /* Readbacks for parity (synchronise). */
 /* rows: n row ids (table-local) of ctx table position t -> out [n, dim] fp32. */
 AS_API as_status as_read_rows(as_ctx* ctx, int32_t t, const int64_t* rows, int64_t n, float* out);

@@ -115,6 +115,9 @@ class Oracle:
         L.orc_emb_forward_f64.argtypes = [C.c_int, C.POINTER(TableC), C.c_int64,
                                           C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                           C.POINTER(C.c_void_p), C.c_uint64, C.POINTER(C.c_double)]
+        L.orc_emb_forward_f64_rows.argtypes = [C.c_int, C.POINTER(TableC), C.c_int64, C.c_int64, C.c_int64,
+                                               C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                               C.POINTER(C.c_void_p), C.c_uint64, C.POINTER(C.c_double)]
         L.orc_emb_backward_adagrad_f64.argtypes = [
             C.POINTER(TableC), C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
             C.POINTER(C.c_float), C.c_int64, C.c_int64, C.POINTER(C.c_float), C.POINTER(C.c_float),
@@ -211,8 +214,9 @@ class Oracle:
         f = self.lib.orc_grad_init
         return np.array([[f(seed, b, c) for c in range(ncols)] for b in range(B)], dtype=np.float32)
 
-    def forward_f64(self, tables, B, streams, wseed=0, dense=None):
-        """streams: list of (offsets, indices) in `tables` order. Returns [B, sum(dim)] fp64."""
+    def forward_f64(self, tables, B, streams, wseed=0, dense=None, rows=None):
+        """streams: list of (offsets, indices) in `tables` order. Returns [B, sum(dim)] fp64
+        (rows=(b0, b1): only those batch rows, [b1 - b0, sum(dim)]; OpenMP)."""
         T = len(tables)
         offs = [np.ascontiguousarray(s[0], dtype=np.int64) for s in streams]
         idxs = [np.ascontiguousarray(s[1], dtype=np.int64) for s in streams]
@@ -222,8 +226,10 @@ class Oracle:
         if dense is not None:
             dense = [np.ascontiguousarray(w, dtype=np.float32) for w in dense]
             pw = (C.c_void_p * T)(*[w.ctypes.data for w in dense])
-        out = np.empty((B, sum(t.dim for t in tables)), dtype=np.float64)
-        self.lib.orc_emb_forward_f64(T, tables_to_c(tables), B, po, pi, pw, wseed, _p(out, C.c_double))
+        b0, b1 = rows if rows is not None else (0, B)
+        out = np.empty((b1 - b0, sum(t.dim for t in tables)), dtype=np.float64)
+        self.lib.orc_emb_forward_f64_rows(T, tables_to_c(tables), B, b0, b1, po, pi, pw, wseed,
+                                          _p(out, C.c_double))
         return out
 
     def backward_adagrad_f64(self, table, B, offsets, indices, grad, col0, lr, eps,

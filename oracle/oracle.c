@@ -379,6 +379,13 @@ float orc_weight_init(uint64_t seed, int32_t table_id, int64_t row, int32_t d) {
   return (float)k * 0x1.0p-12f;
 }
 
+/* orc_weight_init with s0 = splitmix64(seed) hoisted out of the loops */
+static inline float winit_s0(uint64_t s0, int32_t table_id, int64_t row, int32_t d) {
+  uint64_t key = ((uint64_t)(uint32_t)table_id << 40) | ((uint64_t)row << 10) | (uint64_t)d;
+  int k = (int)(orc_splitmix64(s0 ^ key) >> 54) - 512;
+  return (float)k * 0x1.0p-12f;
+}
+
 float orc_grad_init(uint64_t seed, int64_t b, int64_t col) {
   uint64_t key = ((uint64_t)b << 20) | (uint64_t)col;
   uint64_t h = orc_splitmix64(orc_splitmix64(seed ^ 0x5eedf00d5eedf00dull) ^ key);
@@ -392,26 +399,45 @@ void orc_fill_weights(uint64_t seed, int32_t table_id, int64_t rows, int32_t dim
     for (int32_t d = 0; d < dim; ++d) out[r * dim + d] = orc_weight_init(seed, table_id, r, d);
 }
 
+/* Sum pooling in fp64 (out[b, col_t + d] = sum over the bag of
+ * W_t[idx, d]; empty bag -> 0), rows [b0, b1) of the batch into out[b - b0, :].
+ * OpenMP over (table, 64-bag chunk); each output element is summed in bag
+ * order. W[t] = NULL uses the counter-hash init of table t (wseed). */
+void orc_emb_forward_f64_rows(int T, const orc_table* tabs, int64_t B, int64_t b0, int64_t b1,
+                              const int64_t* const* offsets, const int64_t* const* indices,
+                              const float* const* W, uint64_t wseed, double* out) {
+  int64_t sum_dim = 0;
+  int64_t* col = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
+  for (int t = 0; t < T; ++t) {
+    col[t] = sum_dim;
+    sum_dim += tabs[t].dim;
+  }
+  (void)B;
+  const uint64_t s0 = orc_splitmix64(wseed);
+  const int64_t CH = 64, nb = b1 - b0, nch = (nb + CH - 1) / CH;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t w = 0; w < (int64_t)T * nch; ++w) {
+    const int t = (int)(w / nch);
+    const int64_t c0 = b0 + (w % nch) * CH, c1 = c0 + CH < b1 ? c0 + CH : b1;
+    const int D = tabs[t].dim;
+    const float* wt = W ? W[t] : NULL;
+    for (int64_t b = c0; b < c1; ++b) {
+      double* o = out + (b - b0) * sum_dim + col[t];
+      for (int d = 0; d < D; ++d) o[d] = 0.0;
+      for (int64_t j = offsets[t][b]; j < offsets[t][b + 1]; ++j) {
+        const int64_t r = indices[t][j];
+        for (int d = 0; d < D; ++d)
+          o[d] += wt ? (double)wt[r * D + d] : (double)winit_s0(s0, tabs[t].id, r, d);
+      }
+    }
+  }
+  free(col);
+}
+
 void orc_emb_forward_f64(int T, const orc_table* tabs, int64_t B, const int64_t* const* offsets,
                          const int64_t* const* indices, const float* const* W, uint64_t wseed,
                          double* out) {
-  int64_t sum_dim = 0;
-  for (int t = 0; t < T; ++t) sum_dim += tabs[t].dim;
-  int64_t col0 = 0;
-  for (int t = 0; t < T; ++t) {
-    const int D = tabs[t].dim;
-    const float* w = W ? W[t] : NULL;
-    for (int64_t b = 0; b < B; ++b) {
-      double* o = out + b * sum_dim + col0;
-      for (int d = 0; d < D; ++d) o[d] = 0.0;
-      for (int64_t j = offsets[t][b]; j < offsets[t][b + 1]; ++j) {
-        int64_t r = indices[t][j];
-        for (int d = 0; d < D; ++d)
-          o[d] += w ? (double)w[r * D + d] : (double)orc_weight_init(wseed, tabs[t].id, r, d);
-      }
-    }
-    col0 += D;
-  }
+  orc_emb_forward_f64_rows(T, tabs, B, 0, B, offsets, indices, W, wseed, out);
 }
 
 static int cmp_u64(const void* a, const void* b) {
@@ -484,42 +510,58 @@ int orc_emb_backward_adagrad_f64(const orc_table* t, int64_t B, const int64_t* o
 /* fp32 OpenMP CPU step (the timed CPU baseline; kind "port")               */
 /* ------------------------------------------------------------------------ */
 
-/* LSD radix sort of 64-bit keys on the low `bits` bits, 11-bit digits. */
-static void radix_sort_u64(uint64_t* a, uint64_t* tmp, int64_t n, int bits) {
+/* Stable LSD radix sort of 64-bit keys on bits [lo, hi), 11-bit digits. */
+static void radix_sort_u64_bits(uint64_t* a, uint64_t* tmp, int64_t n, int lo, int hi) {
   const int R = 11, NB = 1 << R;
-  int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * NB);
+  int64_t cnt[1 << 11];
   uint64_t *src = a, *dst = tmp;
-  for (int sh = 0; sh < bits; sh += R) {
-    memset(cnt, 0, sizeof(int64_t) * NB);
-    for (int64_t i = 0; i < n; ++i) cnt[(src[i] >> sh) & (NB - 1)]++;
+  for (int sh = lo; sh < hi; sh += R) {
+    const int w = hi - sh < R ? hi - sh : R;
+    const uint64_t m = ((uint64_t)1 << w) - 1;
+    memset(cnt, 0, sizeof(int64_t) * (size_t)NB);
+    for (int64_t i = 0; i < n; ++i) cnt[(src[i] >> sh) & m]++;
     int64_t s = 0;
     for (int i = 0; i < NB; ++i) {
       int64_t c = cnt[i];
       cnt[i] = s;
       s += c;
     }
-    for (int64_t i = 0; i < n; ++i) dst[cnt[(src[i] >> sh) & (NB - 1)]++] = src[i];
+    for (int64_t i = 0; i < n; ++i) dst[cnt[(src[i] >> sh) & m]++] = src[i];
     uint64_t* x = src;
     src = dst;
     dst = x;
   }
   if (src != a) memcpy(a, src, sizeof(uint64_t) * (size_t)n);
-  free(cnt);
 }
 
+/* The CPU port's step, every phase parallel over all threads:
+ *  forward  — (table x 256-bag chunk) tasks, fp32 sums in bag order;
+ *  backward — each table's lookups are bucketed by row range (64 buckets of
+ *             the row's high bits; counting pass + stable scatter per (table,
+ *             bag chunk) task), then every (table, bucket) task sorts its keys
+ *             (row << 20 | bag; already in bag order, so a stable sort on the
+ *             row bits alone) and runs the segment sum + exact row-wise Adagrad
+ *             on its own rows (no two tasks touch the same row). */
+#define ORC_NBK 64
 int orc_cpu_step_f32(int T, const int32_t* dims, const int64_t* hash, int64_t B,
                      const int64_t* const* offsets, const int64_t* const* indices, float* W_all,
                      float* M_all, float* out, float lr, float eps, int n_threads) {
   int64_t* woff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
   int64_t* roff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
   int64_t* coff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
-  woff[0] = roff[0] = coff[0] = 0;
+  int64_t* loff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T + 1));
+  int* rbits = (int*)malloc(sizeof(int) * (size_t)(T > 0 ? T : 1));
+  woff[0] = roff[0] = coff[0] = loff[0] = 0;
   for (int t = 0; t < T; ++t) {
     woff[t + 1] = woff[t] + hash[t] * dims[t];
     roff[t + 1] = roff[t] + hash[t];
     coff[t + 1] = coff[t] + dims[t];
+    loff[t + 1] = loff[t] + offsets[t][B];
+    int rb = 0;
+    while ((1ll << rb) < hash[t]) ++rb;
+    rbits[t] = rb;
   }
-  const int64_t SD = coff[T];
+  const int64_t SD = coff[T], Ltot = loff[T];
   int used = 1;
 #ifdef _OPENMP
   if (n_threads > 0) omp_set_num_threads(n_threads);
@@ -546,29 +588,63 @@ int orc_cpu_step_f32(int T, const int32_t* dims, const int64_t* hash, int64_t B,
       }
     }
   }
-  /* backward (grad = out), per table: radix sort (row, bag), segment sum,
-   * exact row-wise Adagrad */
+  /* backward (grad = out): bucket by row range, sort, segment sum, Adagrad */
+  uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(Ltot > 0 ? Ltot : 1));
+  uint64_t* tmp = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(Ltot > 0 ? Ltot : 1));
+  int64_t* cnt = (int64_t*)calloc((size_t)T * (size_t)nch * ORC_NBK, sizeof(int64_t));
+  int64_t* bstart = (int64_t*)malloc(sizeof(int64_t) * ((size_t)T * ORC_NBK + 1));
+#define BSHIFT(t) (rbits[t] > 6 ? rbits[t] - 6 : 0)
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t w = 0; w < (int64_t)T * nch; ++w) { /* count */
+    int t = (int)(w / nch);
+    int64_t b0 = (w % nch) * CH, b1 = b0 + CH < B ? b0 + CH : B;
+    int64_t* c = cnt + w * ORC_NBK;
+    const int sh = BSHIFT(t);
+    for (int64_t j = offsets[t][b0]; j < offsets[t][b1]; ++j) c[indices[t][j] >> sh]++;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
-  for (int t = 0; t < T; ++t) {
+  for (int t = 0; t < T; ++t) { /* exclusive offsets: bucket-major, then bag chunk */
+    int64_t s = loff[t];
+    for (int k = 0; k < ORC_NBK; ++k) {
+      bstart[(int64_t)t * ORC_NBK + k] = s;
+      for (int64_t c = 0; c < nch; ++c) {
+        int64_t* x = cnt + ((int64_t)t * nch + c) * ORC_NBK + k;
+        int64_t v = *x;
+        *x = s;
+        s += v;
+      }
+    }
+  }
+  bstart[(int64_t)T * ORC_NBK] = Ltot;
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int64_t w = 0; w < (int64_t)T * nch; ++w) { /* stable scatter */
+    int t = (int)(w / nch);
+    int64_t b0 = (w % nch) * CH, b1 = b0 + CH < B ? b0 + CH : B;
+    int64_t* c = cnt + w * ORC_NBK;
+    const int sh = BSHIFT(t);
+    for (int64_t b = b0; b < b1; ++b)
+      for (int64_t j = offsets[t][b]; j < offsets[t][b + 1]; ++j) {
+        const uint64_t r = (uint64_t)indices[t][j];
+        keys[c[r >> sh]++] = (r << 20) | (uint64_t)b;
+      }
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t w = 0; w < (int64_t)T * ORC_NBK; ++w) { /* sort + reduce + Adagrad */
+    int t = (int)(w / ORC_NBK);
+    const int64_t a0 = bstart[w], a1 = bstart[w + 1];
+    if (a1 <= a0) continue;
     const int D = dims[t];
-    const int64_t L = offsets[t][B];
-    if (L == 0) continue;
-    uint64_t* k = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)L);
-    uint64_t* tmp = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)L);
-    for (int64_t b = 0; b < B; ++b)
-      for (int64_t j = offsets[t][b]; j < offsets[t][b + 1]; ++j)
-        k[j] = ((uint64_t)indices[t][j] << 20) | (uint64_t)b;
-    int rb = 0;
-    while ((1ll << rb) < hash[t]) ++rb;
-    radix_sort_u64(k, tmp, L, 20 + rb);
-    float* g = (float*)malloc(sizeof(float) * (size_t)D);
+    uint64_t* k = keys + a0;
+    const int64_t n = a1 - a0;
+    radix_sort_u64_bits(k, tmp + a0, n, 20, 20 + BSHIFT(t));
+    float g[1024];
     float* Wt = W_all + woff[t];
     float* Mt = M_all + roff[t];
     int64_t j = 0;
-    while (j < L) {
+    while (j < n) {
       uint64_t r = k[j] >> 20;
       for (int d = 0; d < D; ++d) g[d] = 0.f;
-      while (j < L && (k[j] >> 20) == r) {
+      while (j < n && (k[j] >> 20) == r) {
         const float* gr = out + (int64_t)(k[j] & 0xfffff) * SD + coff[t];
         for (int d = 0; d < D; ++d) g[d] += gr[d];
         ++j;
@@ -578,13 +654,17 @@ int orc_cpu_step_f32(int T, const int32_t* dims, const int64_t* hash, int64_t B,
       float m1 = Mt[r] + sq / (float)D;
       Mt[r] = m1;
       float mult = lr / (sqrtf(m1) + eps);
-      float* w = Wt + r * D;
-      for (int d = 0; d < D; ++d) w[d] -= mult * g[d];
+      float* wr = Wt + r * D;
+      for (int d = 0; d < D; ++d) wr[d] -= mult * g[d];
     }
-    free(g);
-    free(k);
-    free(tmp);
   }
+#undef BSHIFT
+  free(keys);
+  free(tmp);
+  free(cnt);
+  free(bstart);
+  free(loff);
+  free(rbits);
   free(woff);
   free(roff);
   free(coff);

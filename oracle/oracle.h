@@ -89,6 +89,9 @@ float orc_grad_init(uint64_t seed, int64_t b, int64_t col);
 /* Sum-pooled forward in fp64. out is [B, sum_dim] row-major, table columns in
  * the given table order. W[t] is a dense [hash, dim] fp32 table, or NULL to
  * use orc_weight_init(wseed, ...) on the fly. */
+void orc_emb_forward_f64_rows(int T, const orc_table* tabs, int64_t B, int64_t b0, int64_t b1,
+                              const int64_t* const* offsets, const int64_t* const* indices,
+                              const float* const* W, uint64_t wseed, double* out);
 void orc_emb_forward_f64(int T, const orc_table* tabs, int64_t B,
                          const int64_t* const* offsets,
                          const int64_t* const* indices, const float* const* W,

@@ -6,7 +6,7 @@ device side is hand-written sm_100a CUDA. Importing this package loads the
 native library and raises if it has not been built.
 """
 from ._capi import LIB_PATH, lib
-from .device import BenchConfig, EmbeddingShard, measure_plan
+from .device import BenchConfig, EmbeddingShard, measure_plan, probe_gather_bw
 from .errors import (ConfigError, CudaError, Error, GuardError, IndexError_, InfeasibleError, LookupError_,
                      NcclError, OffsetError, ParseError, ShapeError, StateError)
 from .planners import (HeuristicKind, degree_of_balance, greedy_shard, heuristic_cost, heuristic_name, load_plan,

@@ -121,6 +121,7 @@ SIGNATURES = {
     "as_profile_enable": (i32, [vp, i32]),
     "as_profile_read": (i32, [vp, P(f64), P(i64), i32]),
     "as_table_features": (i32, [vp, P(f64), vp]),
+    "as_probe_gather_bw": (i32, [i32, i64, i32, P(f64)]),
     "as_read_rows": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_momentum": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_buffer": (i32, [vp, i32, vp, i64]),

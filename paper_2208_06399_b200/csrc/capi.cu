@@ -524,4 +524,11 @@ AS_API as_status as_write_table(as_ctx* ctx, int32_t t, const float* w, const fl
   });
 }
 
+AS_API as_status as_probe_gather_bw(int32_t device, int64_t footprint_bytes, int32_t row_bytes, double* gbs) {
+  return guard([&] {
+    need(gbs, "gbs");
+    *gbs = asb::probe_gather_bw(device, footprint_bytes, row_bytes);
+  });
+}
+
 }  // extern "C"

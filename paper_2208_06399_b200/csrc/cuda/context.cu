@@ -12,7 +12,6 @@
 //   pooled fp32 [B, sum dim_t], table columns in context order
 #include "context.hpp"
 #include "kernels.cuh"
-#include "seg_tma.cuh"
 
 #include "sort.cuh"
 
@@ -307,13 +306,6 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
   }
-  if (const char* e = std::getenv("ASB_TMA")) use_tma_ = std::atoi(e) != 0 && !w_half_;
-  cuda_check(cudaFuncSetAttribute(seg_reduce_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kTmaSmemBytes),
-             "tma smem");
-  cuda_check(cudaFuncSetAttribute(seg_reduce_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kTmaSmemBytes),
-             "tma smem");
   cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
@@ -338,6 +330,9 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
 }
 
 EmbContext::~EmbContext() {
+  // a staged job may still be narrowing into / copying from the slot buffers
+  for (Slot& sl : slots_)
+    if (sl.job.joinable()) sl.job.join();
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device_);
@@ -512,17 +507,11 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
     L += n_idx[t];
     nch += units * R;
   }
-  // warp units: tables on the TMA path (rows >= 100 floats) first, one launch each
-  for (int pass = 0; pass < 2; ++pass)
-    for (int t = 0; t < T_; ++t) {
-      const bool tma = use_tma_ && kind_gl(sl.tabs[t].kind) == 32;
-      if (tma != (pass == 0)) continue;
-      sl.tabs[t].unit_off = static_cast<int>(nun);
-      nun += units_of[t];
-    }
-  sl.n_tma_units = 0;
-  for (int t = 0; t < T_; ++t)
-    if (use_tma_ && kind_gl(sl.tabs[t].kind) == 32) sl.n_tma_units += units_of[t];
+  // warp units in table order
+  for (int t = 0; t < T_; ++t) {
+    sl.tabs[t].unit_off = static_cast<int>(nun);
+    nun += units_of[t];
+  }
   if (L >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: a shard takes at most 2^31-1 lookups per batch");
   if (nch >= (1LL << 31)) fail(AS_SHAPE, "as_load_streams: too many chunks");
   sl.L = L;
@@ -797,7 +786,7 @@ void EmbContext::commit(cudaStream_t s) {
   L_ = sl.L;
   n_chunks_ = sl.nch;
   n_units_ = sl.nun;
-  n_tma_units_ = sl.n_tma_units;
+  bag_valid_ = false;  // K4 of this batch has not run yet
   loaded_ = true;
 }
 
@@ -837,27 +826,17 @@ SegParams EmbContext::seg_params(bool fwd) const {
   return p;
 }
 
-// K1 / K3 launches: the TMA-gather kernel for the units of wide-row tables,
-// the register-gather kernel for the rest.
+// K1 / K3 launch: one warp per unit, every lane layout in one launch.
 template <bool FWD>
 void EmbContext::launch_seg(SegParams p, cudaStream_t s) {
-  if (n_tma_units_ > 0) {
-    p.unit_begin = 0;
-    seg_reduce_tma_kernel<FWD><<<grid_for(n_tma_units_, kTmaWarps), kTmaWarps * 32, kTmaSmemBytes, s>>>(
-        p, (int)n_tma_units_);
-    cuda_check(cudaGetLastError(), "seg_reduce_tma_kernel");
-    ++launches_;
-  }
-  if (n_units_ > n_tma_units_) {
-    p.unit_begin = (int)n_tma_units_;
-    if (FWD && w_half_)
-      seg_reduce_kernel<true, true><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(
-          p);
-    else
-      seg_reduce_kernel<FWD><<<grid_for(n_units_ - n_tma_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
-    cuda_check(cudaGetLastError(), "seg_reduce_kernel");
-    ++launches_;
-  }
+  if (n_units_ == 0) return;
+  p.unit_begin = 0;
+  if (FWD && w_half_)
+    seg_reduce_kernel<true, true><<<grid_for(n_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
+  else
+    seg_reduce_kernel<FWD><<<grid_for(n_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);
+  cuda_check(cudaGetLastError(), "seg_reduce_kernel");
+  ++launches_;
 }
 
 void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
@@ -872,6 +851,7 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
                                                                             target, sum_dim_, peers_);
     cuda_check(cudaGetLastError(), "bag_expand_kernel");
     ++launches_;
+    bag_valid_ = true;
   }
   if (n_chunks_ == 0) return;
   if (!prof_serial_) {
@@ -907,6 +887,16 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
 // a side stream right after K4 where it overlaps the forward gather; the
 // backward joins on it (or sorts inline when no forward ran since the load).
 void EmbContext::launch_sort(cudaStream_t s) {
+  if (!bag_valid_ && T_ > 0) {
+    // no forward since this batch was committed: the sort's values (bag ids)
+    // come from K4 in ids-only mode (no pooled rows written)
+    const long long nb = (long long)T_ * B_;
+    bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
+                                                                            nullptr, sum_dim_, PeerOut{});
+    cuda_check(cudaGetLastError(), "bag_expand_kernel");
+    ++launches_;
+    bag_valid_ = true;
+  }
   Phase ph(this, 3, s);
   if (sort_passes_ == 0) return;
   SortParams sp;
@@ -1019,6 +1009,9 @@ double EmbContext::measure(int warmup, int measure, int trim, bool flush, float 
   check();
   require_loaded("as_measure");
   DeviceGuard g(device_);
+  // order the measurement after every earlier use of this context (staged
+  // copies, async steps on other streams, shared scratch)
+  cuda_check(cudaDeviceSynchronize(), "measure: drain prior work");
   cudaStream_t s;
   cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * measure));

@@ -15,6 +15,8 @@
 namespace asb {
 
 void cuda_check(cudaError_t e, const char* what);
+// probe.cu: random-row gather GB/s over `footprint` bytes (roofline denominator)
+double probe_gather_bw(int device, int64_t footprint, int row_bytes);
 
 class EmbContext {
  public:
@@ -99,7 +101,7 @@ class EmbContext {
     int64_t cap = 0;
     std::vector<DevTable> tabs;  // per-batch table layout (lookups, chunks, units)
     std::vector<int> utab;
-    int64_t L = 0, nch = 0, nun = 0, n_tma_units = 0;
+    int64_t L = 0, nch = 0, nun = 0;
     long long* d_raw = nullptr;  // int64 pieces narrowed on the GPU
     int64_t raw_cap = 0;
     bool raw_used = false;
@@ -151,13 +153,12 @@ class EmbContext {
   unsigned fixup_lane_grid_ = 592;
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
-  int64_t n_tma_units_ = 0;
+  bool bag_valid_ = false;  // bag_ holds the current batch's bag ids (K4 ran since the commit)
   PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
   int raw_eighths_ = 0;  // ASB_RAW_EIGHTHS: eighths of the index pieces narrowed on the GPU
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
   double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
   double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)
-  bool use_tma_ = false;  // ASB_TMA=1: TMA bulk-copy gathers for wide rows (measured 3x slower)
   float* carry_ = nullptr;
 
   cudaStream_t side_ = nullptr;  // K2 sort overlapped with the forward

@@ -937,6 +937,7 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
     const int bj = __shfl_sync(0xffffffffu, b, lo);
     if (j < last) bag[j] = bj;
   }
+  if (out == nullptr) return;  // ids only (backward without a forward of this batch)
   unsigned empty = __ballot_sync(0xffffffffu, w0 + lane < nb && o == e);
   while (empty) {
     const int i = __ffs(empty) - 1;

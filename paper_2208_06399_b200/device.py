@@ -114,10 +114,15 @@ class EmbeddingShard:
 
     def stage(self, streams) -> None:
         """Asynchronously copy the next batch to the device (see as_stage_streams)."""
+        # the native staging job reads the host arrays until the matching commit:
+        # keep them (the Workload object or the converted arrays) alive until then
         if isinstance(streams, Workload):
             check(lib().as_stage_workload(self._h, streams.handle))
+            self._staged_keep = getattr(self, "_staged_keep", [])[-1:] + [streams]
             return
         st = [(np.ascontiguousarray(o, dtype=np.int64), np.ascontiguousarray(i, dtype=np.int64)) for o, i in streams]
+        if len(st) != len(self.tables):
+            raise ValueError(f"expected {len(self.tables)} streams, got {len(st)}")
         n = max(1, len(st))
         po = (C.c_void_p * n)(*[o.ctypes.data for o, _ in st])
         pi = (C.c_void_p * n)(*[i.ctypes.data for _, i in st])
@@ -235,6 +240,14 @@ class EmbeddingShard:
             }
 
         return torch.as_tensor(_CAI(), device=f"cuda:{self.device}")
+
+
+def probe_gather_bw(footprint_bytes: int, row_bytes: int, device: int = 0) -> float:
+    """GB/s of random row gathers over a device buffer (as_probe_gather_bw): the
+    measured gather ceiling bench.py reports the seg_reduce kernels against."""
+    g = C.c_double()
+    check(lib().as_probe_gather_bw(int(device), int(footprint_bytes), int(row_bytes), C.byref(g)))
+    return g.value
 
 
 def measure_plan(plan: ShardingPlan, task: ShardingTask, wl: Workload, bench: Optional[BenchConfig] = None,

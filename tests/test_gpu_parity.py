@@ -575,3 +575,23 @@ def test_cfg4_shard_full_size_properties(P, cuda):
                 g = G[bags[order[bounds[k]:bounds[k + 1]]]].sum(0)
                 want = (g @ g) / tab.dim
                 assert abs(mom[q] - want) <= 1e-5 * want + 1e-30, (tab.id, rows[k], counts[k])
+
+
+def test_backward_without_forward_after_load(P, oracle, cuda):
+    """as_backward_rowwise_adagrad straight after a load (no as_forward of this
+    batch): the sort's bag ids must come from THIS batch (K4 runs in ids-only
+    mode), not from the previous batch's forward."""
+    torch = cuda
+    pool = P.generate_pool(2, 6, P.GeneratorConfig(dim_choices=(16, 64), hash_size_max=2e4))
+    B, seed = 700, 21
+    wl_a = P.generate_workload(1, pool, B)
+    wl_b = P.generate_workload(2, pool, B)
+    st_b = streams_of(wl_b, pool)
+    grad = grad_grid(5, B, sum(t.dim for t in pool))
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as sh:
+        sh.load(wl_a)
+        sh.forward()  # bag ids of batch A in the device buffers
+        sh.load(st_b)
+        sh.backward(torch.from_numpy(grad).cuda(), LR, EPS)
+        torch.cuda.synchronize()
+        run_bwd_check(oracle, sh, pool, st_b, grad, seed, B)

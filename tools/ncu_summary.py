@@ -3,6 +3,8 @@
 
 usage: python tools/ncu_summary.py <report.ncu-rep> <out.txt> [workload]
 Maps kernel names to bench.py phases so bench.py can report `roofline.traffic`.
+Each workload's entry is stamped with bench.sources_sha() of the sources the
+capture ran on; bench.py ignores an entry whose stamp does not match.
 """
 import csv
 import io
@@ -10,6 +12,8 @@ import json
 import os
 import subprocess
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
@@ -59,12 +63,15 @@ def main():
             lines.append(f"  {'dram bytes (r+w)':26s} {tot:20.0f} byte")
             for k, ph in PHASE.items():
                 if k in name:
-                    traffic[ph] = {"dram_bytes_per_launch": tot, "report": os.path.basename(rep)}
+                    # first launch of each phase (a capture may hold several steps)
+                    traffic.setdefault(ph, {"dram_bytes_per_launch": tot, "summary": os.path.basename(out)})
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out), "ncu_traffic.json")
+    from bench import sources_sha
+
     d = json.load(open(tj)) if os.path.exists(tj) else {}
-    d.setdefault(workload, {}).update(traffic)
+    d[workload] = {"sources_sha": sources_sha(), "report": os.path.basename(rep), "kernels": traffic}
     json.dump(d, open(tj, "w"), indent=1)
     print("\n".join(lines))
 
