@@ -295,6 +295,9 @@ def main():
     ap.add_argument("--plan-shard", type=int, default=-1,
                     help="N=1: run only this shard of the --plan-k GPU plan (AutoShard-RL if present)")
     ap.add_argument("--plan-k", type=int, default=8)
+    ap.add_argument("--exchange", choices=["peer", "peer-fwd", "nccl"], default="peer",
+                    help="N>1 pooled-row exchange: peer memory both ways (fused forward), fused forward + NCCL "
+                         "backward, or NCCL both ways")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
@@ -329,8 +332,6 @@ def main():
 
     tables_all, B, wdesc = build_workload(P, wname)
     if world > 1:
-        if B % world:
-            raise SystemExit("batch must divide by the GPU count")
         task = device_task(P, tables_all, world, args.weights)
         plan, plan_name = bench_plan(P, task, wname, world)
         mine = [t for t, k in zip(tables_all, plan.assignment) if k == rank]
@@ -355,48 +356,31 @@ def main():
     SD = shard.sum_dim
     pooled = shard.pooled_tensor()
 
-    # N>1: table-wise shards; pooled rows go to their sample owners and the
-    # gradient comes back with the inverse all-to-all (paper_2208_06399_b200.sharded)
+    # N>1: table-wise shards through the C-ABI's sharded step (as_comm,
+    # csrc/cuda/sharded.cu): pooled rows go to their sample owners (forward
+    # exchange fused into the forward kernel's epilogues over peer memory, or
+    # NCCL), the gradient comes back with the inverse exchange, K2/K3 run on
+    # the table owner
     exchange = None
+    comm = None
     if world > 1:
-        from paper_2208_06399_b200.sharded import FusedPooledExchange, PooledExchange, a2a_layout
+        from paper_2208_06399_b200.sharded import a2a_layout, connect
 
         lay = a2a_layout(task, plan, B)
-        exch = None
-        if os.environ.get("ASB_FUSED_A2A", "1") != "0":
-            try:  # forward exchange fused into the forward kernel (peer stores, symmetric memory)
-                exch = FusedPooledExchange(lay, rank, shard, device="cuda")
-                exchange = "fused: pooled rows stored into the sample owners' symmetric-memory receive buffers by the " \
-                           "forward kernel + device barrier; backward: NCCL all_to_all_single"
-            except Exception as e:  # noqa: BLE001
-                exchange = (f"NCCL all_to_all_single both ways (symmetric memory unavailable: "
-                            f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''})")
-        if exch is None:
-            exch = PooledExchange(lay, rank, device="cuda")
-            exchange = exchange or "NCCL all_to_all_single both ways"
+        modes = {"peer": 0, "peer-fwd": 2, "nccl": 3}
+        mode = modes[args.exchange] if not one_gpu else 0
+        comm = connect(shard, lay, rank, world, mode=mode, use_nccl=not one_gpu)
+        exchange = {
+            0: "forward fused into K4/K1 epilogues (NVLink peer stores into the owners' receive buffers) + "
+               "system-scope device barrier; backward: gradient blocks pushed to the table owners by copy engines "
+               "over peer memory + barrier",
+            2: "forward fused into K4/K1 epilogues (peer stores) + device barrier; backward: NCCL send/recv",
+            3: "NCCL grouped send/recv both ways",
+        }[mode] + f" (as_step_sharded; samples split {lay.row_start[1] - lay.row_start[0]}..{lay.rows(world - 1)} per rank)"
 
-    xev = []  # (fwd a, fwd b, bwd a, bwd b) exchange events of the profiling pass
-
-    def step(timed_exchange=False):
+    def step():
         if world > 1:
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timed_exchange else None
-            if isinstance(exch, FusedPooledExchange):
-                recv = exch.forward(stream=stream)  # exchange inside K1/K4 + barrier
-            else:
-                shard.forward(pooled, stream=stream)
-                if ev:
-                    ev[0].record(stream)
-                recv = exch.forward(pooled)
-                if ev:
-                    ev[1].record(stream)
-            # dense part out of scope: loss 1/2|pooled|^2 -> dL/dpooled = pooled (recv)
-            if ev:
-                ev[2].record(stream)
-            g = exch.backward(recv)
-            if ev:
-                ev[3].record(stream)
-                xev.append(ev)
-            shard.backward(g, LR, EPS, stream=stream)
+            comm.step(LR, EPS, stream=stream)  # dense part out of scope: loss 1/2|recv|^2, grad = recv
         else:
             shard.forward(pooled, stream=stream)
             shard.backward(pooled, LR, EPS, stream=stream)
@@ -445,23 +429,26 @@ def main():
     shard.profile(True, serialize=True)
     for i in range(K):
         flush_buf.fill_(float(i))
-        step(timed_exchange=True)
+        step()
     torch.cuda.synchronize()
     exchange_stats = None
-    if world > 1 and xev:
-        # NCCL convention: busbw = (bytes one rank sends / t) * (G-1)/G; max t over ranks
-        bwd_ms = sum(e[2].elapsed_time(e[3]) for e in xev) / len(xev)
-        fwd_ms = (sum(e[0].elapsed_time(e[1]) for e in xev) / len(xev)
-                  if not isinstance(exch, FusedPooledExchange) else None)
-        tx = torch.tensor([bwd_ms, fwd_ms or 0.0], device="cuda", dtype=torch.float64)
+    if world > 1:
+        fwd_x, bwd_x = comm.profile_read(reset=True)
+        tx = torch.tensor([fwd_x / K, bwd_x / K], device="cuda", dtype=torch.float64)
         dist.all_reduce(tx, op=dist.ReduceOp.MAX)
-        bwd_ms, fwd_max = float(tx[0]), float(tx[1])
-        nbytes = 4 * B * max(lay.shard_dims)  # the largest owner's pooled block
-        busbw = lambda ms: round(nbytes / (ms / 1e3) / 1e9 * (world - 1) / world, 1) if ms > 0 else None
-        exchange_stats = {"bwd_a2a_ms": round(bwd_ms, 4), "bwd_busbw_gbs": busbw(bwd_ms),
-                          "fwd_a2a_ms": round(fwd_max, 4) if fwd_ms is not None else "fused into K1/K4 (peer stores)",
-                          "fwd_busbw_gbs": busbw(fwd_max) if fwd_ms is not None else None,
-                          "bytes_per_rank_max": nbytes * (world - 1) // world}
+        ci = comm.info()
+        nb = torch.tensor([float(ci.bytes_sent_fwd), float(ci.bytes_sent_bwd)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(nb, op=dist.ReduceOp.MAX)
+        fwd_ms, bwd_ms = float(tx[0]), float(tx[1])
+        # NCCL convention: busbw of a rank = bytes it sends to the others / t (max t, max bytes over ranks)
+        busbw = lambda nbytes, ms: round(nbytes / (ms / 1e3) / 1e9, 1) if ms > 0 else None
+        exchange_stats = {"fwd_exchange_ms": round(fwd_ms, 4), "bwd_exchange_ms": round(bwd_ms, 4),
+                          "fwd_bytes_per_rank_max": int(nb[0]), "bwd_bytes_per_rank_max": int(nb[1]),
+                          "fwd_busbw_gbs": busbw(float(nb[0]), fwd_ms) if mode & 1 else None,
+                          "bwd_busbw_gbs": busbw(float(nb[1]), bwd_ms),
+                          "note": ("fwd_exchange_ms of the fused forward is the device-barrier wait after K1 (the "
+                                   "peer stores ride in K1/K4); it includes waiting for the slowest rank"
+                                   if not mode & 1 else "NCCL send/recv time")}
     phase_ms, _ = shard.profile_read(reset=True)
     shard.profile(False)
     # shard time = this rank's own kernels (serialized phases, no exchange): the
@@ -525,8 +512,7 @@ def main():
 
         def e2e_step():
             if world > 1:
-                step()
-                return torch.dot(exch.recv_buf, exch.recv_buf).mul_(0.5).item()
+                return comm.step(LR, EPS, want_loss=True, stream=stream)
             return shard.step(LR, EPS, want_loss=True, stream=stream)
 
         shard.stage(wl)
@@ -603,6 +589,8 @@ def main():
                                        round(max(step_ms), 4)],
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     shard.close()
     if world > 1:
         dist.destroy_process_group()

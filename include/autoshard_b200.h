@@ -225,6 +225,13 @@ AS_API as_status as_forward(as_ctx* ctx, float* out_or_null, void* stream);
  * AS_SHAPE unless n_peers * rows_per_peer == batch; at most 8 peers. */
 AS_API as_status as_set_peer_outputs(as_ctx* ctx, int n_peers, float* const* peer_bases, int64_t rows_per_peer);
 
+/* as_set_peer_outputs with UNEVEN sample ranges: peer q owns batch rows
+ * [row_start[q], row_start[q+1]) (row_start[0] = 0, row_start[n_peers] = batch,
+ * nondecreasing), pooled row b of this shard is stored at
+ *   peer_bases[q] + (b - row_start[q]) * sum_dim + col_t. */
+AS_API as_status as_set_peer_outputs_v(as_ctx* ctx, int n_peers, float* const* peer_bases,
+                                       const int64_t* row_start);
+
 /* K2+K3: sort (row, bag), segment-sum the gradient rows per unique row and
  * apply exact row-wise Adagrad in place:
  *   m_r += |g_r|^2 / dim ;  W_r -= lr * g_r / (sqrt(m_r) + eps).
@@ -252,6 +259,95 @@ AS_API as_status as_measure_plan(const as_table_spec* tables, int32_t n, int32_t
                                  const int32_t* assignment, const as_workload* wl,
                                  const int32_t* devices, int32_t n_devices,
                                  const as_bench_config* bench, double* costs);
+
+/* ---------------------------------------------------------------------- */
+/* L4 — table-wise sharded step over G processes, one per GPU             */
+/*      (SURVEY.md §8e). Replaces the pooled-row          */
+/*      all-to-all around the embedding operator.                          */
+/* ---------------------------------------------------------------------- */
+typedef struct as_comm as_comm;
+
+#define AS_UNIQUE_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+#define AS_HANDLE_BYTES 512    /* as_alltoall_handle blob (>= what it writes) */
+
+/* Exchange modes of as_alltoall_setup (bit flags). Without a flag a direction
+ * goes over peer memory:
+ *   forward  — fused into K4/K1's epilogues: pooled rows are stored straight
+ *              into the sample owners' receive buffers (NVLink stores), then a
+ *              system-scope release/acquire device barrier;
+ *   backward — each gradient block is pushed into its table owner's gradient
+ *              buffer by the copy engines (peer memory), then the barrier.
+ * With the flag that direction is a grouped ncclSend / ncclRecv all-to-all
+ * (needs an NCCL communicator). */
+#define AS_XCHG_PEER 0
+#define AS_XCHG_FWD_NCCL 1
+#define AS_XCHG_BWD_NCCL 2
+#define AS_XCHG_NCCL 3
+
+/* ncclGetUniqueId: rank 0 calls it and hands the 128 bytes to every rank.
+ * NCCL is loaded at run time (libnccl.so.2; the one torch loaded if present):
+ * AS_NCCL when it cannot be loaded. */
+AS_API as_status as_comm_unique_id(void* unique_id_out);
+
+/* One rank of a G-rank sharded execution, bound to ctx (this rank's shard of
+ * tables on its device). unique_id != NULL: an NCCL communicator of the G ranks
+ * (ncclCommInitRank; collective: every rank must call it) — peer-memory
+ * handles are then exchanged over it. unique_id == NULL: no NCCL (AS_XCHG_PEER
+ * only); the caller moves the handle blobs itself (as_alltoall_handle /
+ * as_alltoall_open: all-gather them with MPI, torch.distributed, files ...).
+ * 1 <= world <= 8. ctx must outlive the comm. */
+AS_API as_status as_comm_init(as_ctx* ctx, const void* unique_id_or_null, int32_t rank, int32_t world,
+                              as_comm** out);
+AS_API as_status as_comm_destroy(as_comm* comm);
+
+/* Layout of the pooled-row all-to-all: rank k's shard has shard_dims[k] pooled
+ * columns (its tables in ctx order); sample owner p holds batch rows
+ * [row_start[p], row_start[p+1]) (uneven splits allowed; row_start[0] = 0,
+ * row_start[world] = batch). Allocates this rank's receive buffer (world
+ * blocks, block k = [rows_p, shard_dims[k]] fp32, in rank order), its gradient
+ * buffer [batch, shard_dims[rank]] and the barrier flags. With an NCCL comm it
+ * also all-gathers the peer handles (collective), and the exchange is ready;
+ * without, call as_alltoall_handle / as_alltoall_open next. AS_SHAPE when the
+ * layout does not match the ctx (shard_dims[rank] != sum of its dims, batch). */
+AS_API as_status as_alltoall_setup(as_comm* comm, const int64_t* shard_dims, const int64_t* row_start,
+                                   int32_t mode);
+/* This rank's handle blob (cudaIpc handles of its receive / gradient / flag
+ * buffers); *nbytes <= AS_HANDLE_BYTES. */
+AS_API as_status as_alltoall_handle(as_comm* comm, void* blob_out, int64_t* nbytes);
+/* all_blobs: world blobs of AS_HANDLE_BYTES each, in rank order. Opens the
+ * peers' buffers (cudaIpcOpenMemHandle, peer access enabled lazily) and
+ * points this ctx's forward at the owners' receive blocks. */
+AS_API as_status as_alltoall_open(as_comm* comm, const void* all_blobs);
+
+/* The sharded forward: K4/K1 of this rank's tables with every pooled row
+ * delivered to its sample owner, then the exchange barrier (AS_XCHG_PEER) or
+ * the NCCL all-to-all; on return (stream order) this rank's receive buffer
+ * holds the pooled rows of its samples for ALL tables. */
+AS_API as_status as_forward_sharded(as_comm* comm, void* stream);
+/* The sharded backward: grad_recv (device, the receive buffer's layout; NULL =
+ * the receive buffer itself, i.e. loss 1/2 |recv|^2) goes back to the table
+ * owners (inverse all-to-all), then K2/K3 + row-wise Adagrad on this shard. */
+AS_API as_status as_backward_sharded(as_comm* comm, const float* grad_recv_or_null, float lr, float eps,
+                                     void* stream);
+/* as_forward_sharded + loss 1/2 |recv|^2 of this rank's samples (if loss_out:
+ * computed on the device and copied to host, which synchronises) +
+ * as_backward_sharded(grad = recv). */
+AS_API as_status as_step_sharded(as_comm* comm, float lr, float eps, double* loss_out, void* stream);
+
+typedef struct as_comm_info {
+  int32_t rank, world, mode, has_nccl;
+  int64_t recv_rows;     /* rows_p of this rank */
+  int64_t recv_cols;     /* sum_k shard_dims[k] */
+  float* recv;           /* device [world blocks of [rows_p, shard_dims[k]]] */
+  float* grad;           /* device [batch, shard_dims[rank]] */
+  int64_t bytes_sent_fwd;   /* pooled-row bytes this rank sends to OTHER ranks per forward */
+  int64_t bytes_sent_bwd;   /* gradient bytes this rank sends to other ranks per backward */
+} as_comm_info;
+AS_API as_status as_comm_info_get(const as_comm* comm, as_comm_info* info);
+/* Per-step exchange timing (CUDA events on the launching stream, when the
+ * ctx's profiling is on): ms[0] forward exchange (barrier wait, or the NCCL
+ * all-to-all), ms[1] backward exchange; accumulated until reset. */
+AS_API as_status as_comm_profile_read(as_comm* comm, double* ms2, int32_t reset);
 
 /* Introspection for hosts that drive collectives themselves. */
 typedef struct as_ctx_info {

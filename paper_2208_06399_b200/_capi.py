@@ -70,6 +70,23 @@ class CtxInfoC(C.Structure):
     ]
 
 
+class CommInfoC(C.Structure):
+    """as_comm_info."""
+
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("mode", C.c_int32),
+        ("has_nccl", C.c_int32),
+        ("recv_rows", C.c_int64),
+        ("recv_cols", C.c_int64),
+        ("recv", C.c_void_p),
+        ("grad", C.c_void_p),
+        ("bytes_sent_fwd", C.c_int64),
+        ("bytes_sent_bwd", C.c_int64),
+    ]
+
+
 P = C.POINTER
 i32, i64, u64, f32, f64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_void_p
 T_SPEC = P(TableSpecC)
@@ -122,6 +139,18 @@ SIGNATURES = {
     "as_profile_read": (i32, [vp, P(f64), P(i64), i32]),
     "as_table_features": (i32, [vp, P(f64), vp]),
     "as_probe_gather_bw": (i32, [i32, i64, i32, P(f64)]),
+    "as_set_peer_outputs_v": (i32, [vp, i32, P(vp), P(i64)]),
+    "as_comm_unique_id": (i32, [vp]),
+    "as_comm_init": (i32, [vp, vp, i32, i32, P(vp)]),
+    "as_comm_destroy": (i32, [vp]),
+    "as_alltoall_setup": (i32, [vp, P(i64), P(i64), i32]),
+    "as_alltoall_handle": (i32, [vp, vp, P(i64)]),
+    "as_alltoall_open": (i32, [vp, vp]),
+    "as_forward_sharded": (i32, [vp, vp]),
+    "as_backward_sharded": (i32, [vp, vp, f32, f32, vp]),
+    "as_step_sharded": (i32, [vp, f32, f32, P(f64), vp]),
+    "as_comm_info_get": (i32, [vp, P(CommInfoC)]),
+    "as_comm_profile_read": (i32, [vp, P(f64), i32]),
     "as_read_rows": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_momentum": (i32, [vp, i32, P(i64), i64, P(f32)]),
     "as_read_buffer": (i32, [vp, i32, vp, i64]),

@@ -9,6 +9,7 @@
 
 #include "autoshard_b200.h"
 #include "cuda/context.hpp"
+#include "cuda/sharded.hpp"
 #include "host/host.hpp"
 
 struct as_workload {
@@ -16,6 +17,9 @@ struct as_workload {
 };
 struct as_ctx {
   std::unique_ptr<asb::EmbContext> impl;
+};
+struct as_comm {
+  std::unique_ptr<asb::ShardComm> impl;
 };
 
 namespace {
@@ -409,7 +413,24 @@ AS_API as_status as_set_peer_outputs(as_ctx* ctx, int n_peers, float* const* pee
   return guard([&] {
     need(ctx, "ctx");
     if (n_peers > 0) need(peer_bases, "peer_bases");
-    ctx->impl->set_peer_outputs(n_peers, peer_bases, rows_per_peer);
+    if (n_peers < 0 || n_peers > 8) asb::fail(AS_CONFIG, "as_set_peer_outputs: 0..8 peers, got " + std::to_string(n_peers));
+    int64_t starts[9];
+    for (int q = 0; q <= n_peers; ++q) starts[q] = rows_per_peer * q;
+    if (n_peers > 0 && rows_per_peer * n_peers != ctx->impl->batch())
+      asb::fail(AS_SHAPE, "as_set_peer_outputs: " + std::to_string(n_peers) + " peers x " + std::to_string(rows_per_peer) +
+                              " rows must cover the batch of " + std::to_string(ctx->impl->batch()));
+    ctx->impl->set_peer_outputs(n_peers, peer_bases, starts);
+  });
+}
+
+AS_API as_status as_set_peer_outputs_v(as_ctx* ctx, int n_peers, float* const* peer_bases, const int64_t* row_start) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (n_peers > 0) {
+      need(peer_bases, "peer_bases");
+      need(row_start, "row_start");
+    }
+    ctx->impl->set_peer_outputs(n_peers, peer_bases, row_start);
   });
 }
 
@@ -521,6 +542,89 @@ AS_API as_status as_write_table(as_ctx* ctx, int32_t t, const float* w, const fl
   return guard([&] {
     need(ctx, "ctx");
     ctx->impl->write_table(t, w, m);
+  });
+}
+
+AS_API as_status as_comm_unique_id(void* id) {
+  return guard([&] {
+    need(id, "unique_id_out");
+    asb::nccl_unique_id(id);
+  });
+}
+
+AS_API as_status as_comm_init(as_ctx* ctx, const void* uid, int32_t rank, int32_t world, as_comm** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    auto c = std::make_unique<as_comm>();
+    c->impl = std::make_unique<asb::ShardComm>(ctx->impl.get(), uid, rank, world);
+    *out = c.release();
+  });
+}
+
+AS_API as_status as_comm_destroy(as_comm* comm) {
+  return guard([&] { delete comm; });
+}
+
+AS_API as_status as_alltoall_setup(as_comm* comm, const int64_t* shard_dims, const int64_t* row_start, int32_t mode) {
+  return guard([&] {
+    need(comm, "comm");
+    need(shard_dims, "shard_dims");
+    need(row_start, "row_start");
+    comm->impl->setup(shard_dims, row_start, mode);
+  });
+}
+
+AS_API as_status as_alltoall_handle(as_comm* comm, void* blob, int64_t* nbytes) {
+  return guard([&] {
+    need(comm, "comm");
+    need(blob, "blob_out");
+    comm->impl->handle(blob, nbytes);
+  });
+}
+
+AS_API as_status as_alltoall_open(as_comm* comm, const void* all) {
+  return guard([&] {
+    need(comm, "comm");
+    need(all, "all_blobs");
+    comm->impl->open(all);
+  });
+}
+
+AS_API as_status as_forward_sharded(as_comm* comm, void* stream) {
+  return guard([&] {
+    need(comm, "comm");
+    comm->impl->forward(static_cast<cudaStream_t>(stream));
+  });
+}
+
+AS_API as_status as_backward_sharded(as_comm* comm, const float* grad_recv, float lr, float eps, void* stream) {
+  return guard([&] {
+    need(comm, "comm");
+    comm->impl->backward(grad_recv, lr, eps, static_cast<cudaStream_t>(stream));
+  });
+}
+
+AS_API as_status as_step_sharded(as_comm* comm, float lr, float eps, double* loss_out, void* stream) {
+  return guard([&] {
+    need(comm, "comm");
+    comm->impl->step(lr, eps, loss_out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+AS_API as_status as_comm_info_get(const as_comm* comm, as_comm_info* info) {
+  return guard([&] {
+    need(comm, "comm");
+    need(info, "info");
+    comm->impl->info(info);
+  });
+}
+
+AS_API as_status as_comm_profile_read(as_comm* comm, double* ms2, int32_t reset) {
+  return guard([&] {
+    need(comm, "comm");
+    need(ms2, "ms2");
+    comm->impl->profile_read(ms2, reset != 0);
   });
 }
 

@@ -964,21 +964,25 @@ void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s
   launches_ += 3;
 }
 
-void EmbContext::set_peer_outputs(int n, float* const* bases, int64_t rows) {
+void EmbContext::set_peer_outputs(int n, float* const* bases, const int64_t* row_start) {
   if (n == 0) {
     std::memset(&peers_, 0, sizeof peers_);
     return;
   }
   if (n < 0 || n > kMaxPeers) fail(AS_CONFIG, "as_set_peer_outputs: 0..8 peers, got " + std::to_string(n));
-  if (rows < 1 || rows * n != B_)
-    fail(AS_SHAPE, "as_set_peer_outputs: " + std::to_string(n) + " peers x " + std::to_string(rows) +
-                       " rows must cover the batch of " + std::to_string(B_));
-  for (int q = 0; q < n; ++q)
-    if (!bases[q]) fail(AS_CONFIG, "as_set_peer_outputs: peer " + std::to_string(q) + " has a NULL base");
+  if (row_start[0] != 0 || row_start[n] != B_)
+    fail(AS_SHAPE, "as_set_peer_outputs: the peers' row ranges must cover the batch [0, " + std::to_string(B_) + ")");
+  for (int q = 0; q < n; ++q) {
+    if (row_start[q + 1] < row_start[q])
+      fail(AS_SHAPE, "as_set_peer_outputs: row_start must be nondecreasing at peer " + std::to_string(q + 1));
+    if (!bases[q] && row_start[q + 1] > row_start[q])
+      fail(AS_CONFIG, "as_set_peer_outputs: peer " + std::to_string(q) + " has a NULL base");
+  }
   std::memset(&peers_, 0, sizeof peers_);
   for (int q = 0; q < n; ++q) peers_.base[q] = bases[q];
+  for (int q = 0; q <= n; ++q) peers_.start[q] = static_cast<int>(row_start[q]);
+  for (int q = n + 1; q <= kMaxPeers; ++q) peers_.start[q] = static_cast<int>(B_);
   peers_.n = n;
-  peers_.rows = static_cast<int>(rows);
 }
 
 void EmbContext::step(float lr, float eps, double* loss_host, cudaStream_t s) {

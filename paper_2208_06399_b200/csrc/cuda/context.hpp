@@ -34,7 +34,12 @@ class EmbContext {
   void check();
   void forward(float* out, double* loss_dev, cudaStream_t s);
   void backward(const float* grad, float lr, float eps, cudaStream_t s);
-  void set_peer_outputs(int n, float* const* bases, int64_t rows);
+  void set_peer_outputs(int n, float* const* bases, const int64_t* row_start);
+  bool has_peers() const { return peers_.n != 0; }
+  bool profiling() const { return prof_; }
+  int64_t batch() const { return B_; }
+  int64_t sum_dim() const { return sum_dim_; }
+  float* pooled() const { return out_; }
   void step(float lr, float eps, double* loss_host, cudaStream_t s);
   double measure(int warmup, int measure, int trim, bool flush, float lr, float eps);
 

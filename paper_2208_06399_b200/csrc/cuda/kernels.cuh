@@ -177,8 +177,10 @@ __device__ __forceinline__ float group_sum(float x, unsigned mask) {
 // buffer of the sample's owner (fused exchange, PeerOut).
 __device__ __forceinline__ float* pooled_row(float* out, long long stride, const PeerOut& peers, int b) {
   if (peers.n == 0) return out + (long long)b * stride;
-  const int q = b / peers.rows;
-  return peers.base[q] + (long long)(b - q * peers.rows) * stride;
+  int q = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxPeers; ++i) q += (i < peers.n && b >= peers.start[i]) ? 1 : 0;
+  return peers.base[q] + (long long)(b - peers.start[q]) * stride;
 }
 
 // Column group (4 columns) held in slot w of lane c. Standard layouts stride

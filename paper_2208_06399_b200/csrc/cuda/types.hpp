@@ -50,15 +50,15 @@ __host__ __device__ constexpr int kind_nv(int k) { return k <= 5 ? 1 : (k <= 8 ?
 constexpr int kNumKinds = 13;
 
 // Fused forward exchange (table-wise sharding): pooled row b
-// goes straight to the receive buffer of its sample owner q = b / rows, at
-// base[q] + (b - q*rows) * out_stride + col_t — on another GPU a peer
-// (NVLink) store, so the all-to-all of the pooled rows rides on the K1
-// epilogue. n = 0: the plain [B, sum_dim] output.
+// goes straight to the receive buffer of its sample owner q (start[q] <= b <
+// start[q+1]; uneven splits allowed), at base[q] + (b - start[q]) * out_stride
+// + col_t — on another GPU a peer (NVLink) store, so the all-to-all of the
+// pooled rows rides on the K1 epilogue. n = 0: the plain [B, sum_dim] output.
 constexpr int kMaxPeers = 8;
 struct PeerOut {
   float* base[kMaxPeers];
+  int start[kMaxPeers + 1];
   int n;
-  int rows;
 };
 
 struct SegParams {

@@ -142,13 +142,18 @@ class EmbeddingShard:
     def forward(self, out=None, stream=None) -> None:
         check(lib().as_forward(self._h, _ptr(out), _stream(stream)))
 
-    def set_peer_outputs(self, bases, rows_per_peer: int) -> None:
-        """Fused forward exchange (as_set_peer_outputs): pooled row b goes to
-        bases[b // rows_per_peer] (device addresses, e.g. symmetric-memory peer
-        buffers); bases=[] restores the local output."""
+    def set_peer_outputs(self, bases, rows) -> None:
+        """Fused forward exchange (as_set_peer_outputs[_v]): pooled row b goes to
+        bases[q] for the peer q whose sample range holds b. rows: rows per peer
+        (int, even split) or the row_start list (len(bases) + 1 entries, uneven
+        splits); bases=[] restores the local output."""
         n = len(bases)
         arr = (C.c_void_p * max(1, n))(*[int(b) for b in bases])
-        check(lib().as_set_peer_outputs(self._h, n, arr, int(rows_per_peer) if n else 0))
+        if isinstance(rows, int):
+            check(lib().as_set_peer_outputs(self._h, n, arr, int(rows) if n else 0))
+        else:
+            st = (C.c_int64 * (n + 1))(*[int(x) for x in rows]) if n else None
+            check(lib().as_set_peer_outputs_v(self._h, n, arr, st))
 
     def backward(self, grad=None, lr: float = 0.01, eps: float = 1e-8, stream=None) -> None:
         check(lib().as_backward_rowwise_adagrad(self._h, _ptr(grad), lr, eps, _stream(stream)))

@@ -4,23 +4,40 @@ GPU.
 Rank k holds the tables with ``plan.assignment[i] == k`` (positional against
 ``task.tables``, tables.hpp:93-116) and computes their pooled rows for the
 whole global batch B: a [B, SD_k] fp32 block, SD_k = sum of its tables' dims.
-Samples are data-parallel: rank p owns samples [p*B/G, (p+1)*B/G). The
-forward exchange sends rows [p*B/G, (p+1)*B/G) of every table owner's block to
-rank p (one ``all_to_all_single``; the rows are contiguous, so no packing);
-rank p receives G blocks [B/G, SD_k] in rank order. The backward exchange is
-the exact inverse for the gradient of those rows.
+Samples are data-parallel: rank p owns samples [row_start[p], row_start[p+1])
+(B/G each, the first B % G ranks one more). The forward exchange delivers rows
+[row_start[p], row_start[p+1]) of every table owner's block to rank p, whose
+receive buffer holds G blocks [rows_p, SD_k] in rank order; the backward
+exchange is the exact inverse for the gradient of those rows.
 
-The collectives go through ``torch.distributed`` (NCCL over NVLink on the
-GPU box, gloo in the CPU tests). ``FusedPooledExchange`` removes the forward
-collective: the forward kernel itself stores each pooled row into its sample
-owner's receive buffer (torch symmetric memory, peer stores over NVLink).
+``ShardComm`` is the product path: the C-ABI's ``as_comm`` (csrc/cuda/sharded.cu).
+Its forward exchange is fused into the forward kernel (pooled rows stored into
+the owners' receive buffers over peer memory, then a system-scope device
+barrier), its backward pushes each gradient block into its table owner's buffer
+(or either direction over NCCL send/recv). ``PooledExchange`` is the plain
+``torch.distributed.all_to_all_single`` formulation of the same exchange: the
+library baseline and the gloo CPU tests' path.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
 from .tables import ShardingPlan, ShardingTask, TableDesc
+
+UNIQUE_ID_BYTES = 128  # AS_UNIQUE_ID_BYTES
+HANDLE_BYTES = 512  # AS_HANDLE_BYTES
+XCHG_PEER, XCHG_FWD_NCCL, XCHG_BWD_NCCL, XCHG_NCCL = 0, 1, 2, 3
+
+
+def row_starts(batch: int, world: int) -> List[int]:
+    """Sample ranges of the ranks: B // G rows each, the first B % G ranks one more."""
+    base, extra = divmod(batch, world)
+    out = [0]
+    for p in range(world):
+        out.append(out[-1] + base + (1 if p < extra else 0))
+    return out
 
 
 @dataclass
@@ -30,21 +47,22 @@ class A2ALayout:
     shard_dims: List[int]  # SD_k per rank
     shard_tables: List[List[int]]  # positions into task.tables per rank, placement order
     columns: List[List[int]]  # per rank: first pooled column of each member table
+    row_start: List[int]  # sample ranges, world + 1 entries
 
-    @property
-    def rows_per_rank(self) -> int:
-        return self.batch // self.world
+    def rows(self, p: int) -> int:
+        return self.row_start[p + 1] - self.row_start[p]
 
     def send_splits(self, rank: int) -> List[int]:
         """Element counts rank sends to each peer in the forward exchange."""
-        return [self.rows_per_rank * self.shard_dims[rank]] * self.world
+        return [self.rows(q) * self.shard_dims[rank] for q in range(self.world)]
 
-    def recv_splits(self) -> List[int]:
-        """Element counts received from each table owner in the forward exchange."""
-        return [self.rows_per_rank * d for d in self.shard_dims]
+    def recv_splits(self, rank: int) -> List[int]:
+        """Element counts rank receives from each table owner in the forward exchange."""
+        return [self.rows(rank) * d for d in self.shard_dims]
 
-    def recv_offset(self, owner: int) -> int:
-        return self.rows_per_rank * sum(self.shard_dims[:owner])
+    def recv_offset(self, owner: int, rank: int) -> int:
+        """Element offset of owner's block in rank's receive buffer."""
+        return self.rows(rank) * sum(self.shard_dims[:owner])
 
     def locate(self, table_pos: int):
         """(owner rank, first column inside the owner's block) of task.tables[table_pos]."""
@@ -53,12 +71,19 @@ class A2ALayout:
                 return k, self.columns[k][members.index(table_pos)]
         raise KeyError(table_pos)
 
+    def dim_of(self, table_pos: int) -> int:
+        owner, _ = self.locate(table_pos)
+        members = self.shard_tables[owner]
+        k = members.index(table_pos)
+        cols = self.columns[owner] + [self.shard_dims[owner]]
+        return cols[k + 1] - cols[k]
+
 
 def a2a_layout(task: ShardingTask, plan: ShardingPlan, batch: int) -> A2ALayout:
     plan.validate(task)
     world = task.num_shards
-    if batch % world:
-        raise ValueError(f"batch {batch} must divide by the shard count {world}")
+    if batch < world:
+        raise ValueError(f"batch {batch} is smaller than the shard count {world}")
     members = plan.shard_member_indices(task)
     dims = [sum(task.tables[i].dim for i in m) for m in members]
     cols = []
@@ -68,27 +93,37 @@ def a2a_layout(task: ShardingTask, plan: ShardingPlan, batch: int) -> A2ALayout:
             c.append(acc)
             acc += task.tables[i].dim
         cols.append(c)
-    return A2ALayout(world, batch, dims, members, cols)
+    return A2ALayout(world, batch, dims, members, cols, row_starts(batch, world))
 
 
 def local_tables(task: ShardingTask, plan: ShardingPlan, rank: int) -> List[TableDesc]:
     return [task.tables[i] for i in plan.shard_member_indices(task)[rank]]
 
 
+def recv_table_rows(layout: A2ALayout, recv_flat, rank: int, table_pos: int):
+    """[rows_rank, dim] pooled rows of task.tables[table_pos] in rank's receive buffer."""
+    owner, col = layout.locate(table_pos)
+    o = layout.recv_offset(owner, rank)
+    n = layout.rows(rank) * layout.shard_dims[owner]
+    block = recv_flat[o:o + n].reshape(layout.rows(rank), layout.shard_dims[owner])
+    return block[:, col:col + layout.dim_of(table_pos)]
+
+
 class PooledExchange:
-    """Forward / backward all-to-all of pooled rows for one rank."""
+    """Forward / backward all-to-all of pooled rows for one rank with
+    torch.distributed.all_to_all_single (the library formulation)."""
 
     def __init__(self, layout: A2ALayout, rank: int, group=None, device=None):
         import torch
 
         self.L, self.rank, self.group = layout, rank, group
         self.send = layout.send_splits(rank)
-        self.recv = layout.recv_splits()
+        self.recv = layout.recv_splits(rank)
         self.recv_buf = torch.empty(sum(self.recv), dtype=torch.float32, device=device)
         self.grad_buf = torch.empty(layout.batch * layout.shard_dims[rank], dtype=torch.float32, device=device)
 
     def forward(self, pooled):
-        """pooled: this rank's [B, SD_rank] block -> flat receive buffer (G blocks [B/G, SD_k])."""
+        """pooled: this rank's [B, SD_rank] block -> flat receive buffer (G blocks [rows_rank, SD_k])."""
         import torch.distributed as dist
 
         dist.all_to_all_single(self.recv_buf, pooled.reshape(-1), self.recv, self.send, group=self.group)
@@ -101,65 +136,131 @@ class PooledExchange:
         dist.all_to_all_single(self.grad_buf, grad_recv.reshape(-1), self.send, self.recv, group=self.group)
         return self.grad_buf.view(self.L.batch, self.L.shard_dims[self.rank])
 
-    def block(self, recv_flat, owner: int):
-        """View of the [B/G, SD_owner] block received from `owner`."""
-        o = self.L.recv_offset(owner)
-        n = self.L.rows_per_rank * self.L.shard_dims[owner]
-        return recv_flat[o:o + n].view(self.L.rows_per_rank, self.L.shard_dims[owner])
-
     def table_rows(self, recv_flat, table_pos: int):
-        """[B/G, dim] pooled rows of task.tables[table_pos] for this rank's samples."""
-        owner, col = self.L.locate(table_pos)
-        return self.block(recv_flat, owner)[:, col:col + self._dim_of(table_pos)]
-
-    def _dim_of(self, table_pos):
-        owner, _ = self.L.locate(table_pos)
-        members = self.L.shard_tables[owner]
-        k = members.index(table_pos)
-        cols = self.L.columns[owner] + [self.L.shard_dims[owner]]
-        return cols[k + 1] - cols[k]
+        return recv_table_rows(self.L, recv_flat, self.rank, table_pos)
 
 
 def peer_bases(layout: A2ALayout, owner: int, recv_base_ptrs: Sequence[int]) -> List[int]:
-    """Device addresses the owner's forward writes to (as_set_peer_outputs):
-    for every sample owner q, q's receive buffer + this owner's block offset."""
-    return [int(p) + 4 * layout.recv_offset(owner) for p in recv_base_ptrs]
+    """Device addresses owner's forward writes to (as_set_peer_outputs_v):
+    for every sample owner q, q's receive buffer + owner's block offset."""
+    return [int(p) + 4 * layout.recv_offset(owner, q) for q, p in enumerate(recv_base_ptrs)]
 
 
-class FusedPooledExchange:
-    """Forward exchange fused into the forward kernel: the
-    receive buffers live in torch symmetric memory (one allocation per rank,
-    mapped into every peer over NVLink), the shard's K1/K4 epilogues store each
-    pooled row straight into its sample owner's receive block
-    (EmbeddingShard.set_peer_outputs), and a device-side barrier orders the
-    readers. No pooled-row copy, no NCCL call in the forward. The backward
-    exchange of the gradients stays the NCCL all-to-all (PooledExchange).
+# ---------------------------------------------------------------------------
+# the product path: as_comm (C-ABI)
+# ---------------------------------------------------------------------------
+def unique_id() -> bytes:
+    """ncclGetUniqueId through the C-ABI (rank 0 creates, every rank receives)."""
+    from ._capi import lib
+    from .errors import check
 
-    Raises when symmetric memory is unavailable; callers fall back to
-    PooledExchange."""
+    buf = C.create_string_buffer(UNIQUE_ID_BYTES)
+    check(lib().as_comm_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, layout: A2ALayout, rank: int, shard, group=None, device=None):
+
+class ShardComm:
+    """One rank of the sharded step (as_comm): exchange + this rank's shard."""
+
+    def __init__(self, shard, rank: int, world: int, nccl_id: Optional[bytes] = None):
+        from ._capi import lib
+        from .errors import check
+
+        self.shard, self.rank, self.world = shard, rank, world
+        h = C.c_void_p()
+        uid = C.create_string_buffer(nccl_id, UNIQUE_ID_BYTES) if nccl_id is not None else None
+        check(lib().as_comm_init(shard._h, uid, rank, world, C.byref(h)))
+        self._h = h
+        self._lib, self._check = lib, check
+
+    def setup(self, layout: A2ALayout, mode: int = XCHG_PEER) -> None:
+        d = (C.c_int64 * self.world)(*layout.shard_dims)
+        s = (C.c_int64 * (self.world + 1))(*layout.row_start)
+        self._check(self._lib().as_alltoall_setup(self._h, d, s, int(mode)))
+        self.layout = layout
+
+    def handle(self) -> bytes:
+        buf = C.create_string_buffer(HANDLE_BYTES)
+        n = C.c_int64()
+        self._check(self._lib().as_alltoall_handle(self._h, buf, C.byref(n)))
+        return buf.raw
+
+    def open(self, blobs: Sequence[bytes]) -> None:
+        allb = b"".join(bytes(b).ljust(HANDLE_BYTES, b"\0")[:HANDLE_BYTES] for b in blobs)
+        self._check(self._lib().as_alltoall_open(self._h, C.create_string_buffer(allb, len(allb))))
+
+    def forward(self, stream=None) -> None:
+        from .device import _stream
+
+        self._check(self._lib().as_forward_sharded(self._h, _stream(stream)))
+
+    def backward(self, grad_recv=None, lr: float = 0.01, eps: float = 1e-8, stream=None) -> None:
+        from .device import _ptr, _stream
+
+        self._check(self._lib().as_backward_sharded(self._h, _ptr(grad_recv), lr, eps, _stream(stream)))
+
+    def step(self, lr: float = 0.01, eps: float = 1e-8, want_loss: bool = False, stream=None) -> Optional[float]:
+        from .device import _stream
+
+        loss = C.c_double()
+        self._check(self._lib().as_step_sharded(self._h, lr, eps, C.byref(loss) if want_loss else None,
+                                                _stream(stream)))
+        return loss.value if want_loss else None
+
+    def info(self):
+        from ._capi import CommInfoC
+
+        i = CommInfoC()
+        self._check(self._lib().as_comm_info_get(self._h, C.byref(i)))
+        return i
+
+    def profile_read(self, reset: bool = True):
+        """-> (forward exchange ms, backward exchange ms) accumulated while the shard profiles."""
+        ms = (C.c_double * 2)()
+        self._check(self._lib().as_comm_profile_read(self._h, ms, int(reset)))
+        return ms[0], ms[1]
+
+    def recv_tensor(self):
+        """torch view of this rank's receive buffer (flat fp32)."""
         import torch
-        import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm_mem
 
-        self.L, self.rank, self.group = layout, rank, group
-        group = group or dist.group.WORLD
-        n = layout.rows_per_rank * sum(layout.shard_dims)
-        self.recv_buf = symm_mem.empty(n, dtype=torch.float32, device=device)
-        self.hdl = symm_mem.rendezvous(self.recv_buf, group)
-        self.shard = shard
-        shard.set_peer_outputs(peer_bases(layout, rank, self.hdl.buffer_ptrs), layout.rows_per_rank)
-        self._nccl = PooledExchange(layout, rank, group=self.group, device=device)
+        i = self.info()
+        n = int(i.recv_rows * i.recv_cols)
 
-    def forward(self, stream=None):
-        """This rank's forward with the exchange fused in; returns the receive buffer."""
-        self.shard.forward(stream=stream)
-        self.hdl.barrier(channel=0)  # every owner's stores into every receive buffer are done
-        return self.recv_buf
+        class _CAI:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (int(i.recv), False),
+                                        "version": 3, "strides": None}
 
-    def backward(self, grad_recv):
-        return self._nccl.backward(grad_recv)
+        return torch.as_tensor(_CAI(), device=f"cuda:{self.shard.device}")
 
-    def close(self):
-        self.shard.set_peer_outputs([], 0)
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._check(self._lib().as_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def connect(shard, layout: A2ALayout, rank: int, world: int, mode: int = XCHG_PEER, group=None,
+            use_nccl: bool = True) -> ShardComm:
+    """Build this rank's ShardComm with torch.distributed as the control plane:
+    the NCCL unique id (if use_nccl) is broadcast from rank 0; without NCCL
+    the peer-memory handle blobs are all-gathered here instead of over NCCL."""
+    import torch.distributed as dist
+
+    uid = None
+    if use_nccl:
+        obj = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = obj[0]
+    comm = ShardComm(shard, rank, world, uid)
+    comm.setup(layout, mode)
+    if uid is None:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, comm.handle(), group=group)
+        comm.open(blobs)
+    return comm

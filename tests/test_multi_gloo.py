@@ -40,7 +40,7 @@ def _worker(rank, world, port, result_q):
         o = Oracle()
         pool = P.generate_pool(0, 7, P.GeneratorConfig(dim_choices=(16, 32, 64), hash_size_max=2e4,
                                                       pooling_mean_target=10.0))
-        B = 64
+        B = 67  # uneven sample split (B % world != 0)
         task = P.ShardingTask(pool, world, [10 ** 12] * world)
         plan = P.greedy_shard(task, P.HeuristicKind.kLookupGreedy)
         mine = local_tables(task, plan, rank)
@@ -55,7 +55,7 @@ def _worker(rank, world, port, result_q):
         st_all = [(wl_all.find(t.id).offsets, wl_all.find(t.id).indices) for t in pool]
         full = o.forward_f64(to_oracle_tables(pool), B, st_all, wseed=3).astype(np.float32)
         cols = np.cumsum([0] + [t.dim for t in pool])
-        rows = slice(rank * B // world, (rank + 1) * B // world)
+        rows = slice(lay.row_start[rank], lay.row_start[rank + 1])
         ok = True
         for i, t in enumerate(pool):
             got = ex.table_rows(recv, i).numpy()
@@ -94,12 +94,16 @@ def test_layout_splits_and_locate(P):
     assert sum(lay.shard_dims) == sum(t.dim for t in pool)
     for r in range(4):
         assert sum(lay.send_splits(r)) == 4096 * lay.shard_dims[r]
-    assert sum(lay.recv_splits()) == 1024 * sum(t.dim for t in pool)
+    assert sum(lay.recv_splits(0)) == 1024 * sum(t.dim for t in pool)
     for i in range(10):
         k, col = lay.locate(i)
         assert plan.assignment[i] == k
+    odd = a2a_layout(task, plan, 4095)  # uneven: 1024, 1024, 1024, 1023 rows
+    assert odd.row_start == [0, 1024, 2048, 3072, 4095]
+    assert sum(sum(odd.send_splits(r)) for r in range(4)) == 4095 * sum(odd.shard_dims)
+    assert sum(sum(odd.recv_splits(r)) for r in range(4)) == 4095 * sum(odd.shard_dims)
     with pytest.raises(ValueError):
-        a2a_layout(task, plan, 4095)
+        a2a_layout(task, plan, 3)
 
 
 def test_peer_bases_match_receive_layout():
@@ -110,8 +114,8 @@ def test_peer_bases_match_receive_layout():
     pool = P.generate_pool(0, 9, P.GeneratorConfig(dim_choices=(16, 32, 64)))
     task = P.ShardingTask(pool, 3, [1 << 40] * 3)
     plan = P.random_shard(task, 2)
-    lay = a2a_layout(task, plan, 96)
+    lay = a2a_layout(task, plan, 97)  # rows 33, 32, 32
     bases = [1 << 20, 2 << 20, 3 << 20]
     for k in range(3):
         got = peer_bases(lay, k, bases)
-        assert got == [b + 4 * 32 * sum(lay.shard_dims[:k]) for b in bases]
+        assert got == [b + 4 * lay.rows(q) * sum(lay.shard_dims[:k]) for q, b in enumerate(bases)]

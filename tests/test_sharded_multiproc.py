@@ -1,0 +1,120 @@
+"""The sharded step through the C-ABI (as_comm, csrc/cuda/sharded.cu) with
+real processes: each rank's receive buffer, loss and updated rows against the
+fp64 oracle of all tables (tests/sharded_worker.py).
+
+* 2 processes on ONE GPU (the GPU box has one): the peer-memory exchange
+  (cudaIpc-mapped receive / gradient buffers, the fused peer-store forward, the
+  system-scope device barrier, the gradient push) between two processes —
+  NCCL refuses two ranks on one device, so the handles go over gloo.
+* >= 2 GPUs: the same with NCCL as the control plane, for every exchange mode.
+* world 1 with a real NCCL communicator (one GPU): NCCL send/recv in both
+  directions must give bit-identical results to the unsharded step.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world, mode, nccl, one_gpu, timeout=240):
+    port = _port()
+    procs = []
+    for r in range(world):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                   ASB_MODE=str(mode), ASB_NCCL="1" if nccl else "0", ASB_ONE_GPU="1" if one_gpu else "0")
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "sharded_worker.py")], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    res = []
+    for p in procs:
+        try:
+            so, se = p.communicate(timeout=timeout)
+        except subprocess.TimeoutExpired:
+            for q in procs:
+                q.kill()
+            raise
+        assert p.returncode == 0, se[-4000:]
+        res.append(json.loads(so.strip().splitlines()[-1]))
+    return res
+
+
+def test_two_processes_one_gpu_peer_exchange(cuda):
+    res = _run(2, 0, nccl=False, one_gpu=True)
+    for r in res:
+        assert r["ok"], r["errors"]
+        assert r["bytes_sent_fwd"] > 0 and r["bytes_sent_bwd"] > 0
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_multi_gpu_sharded_step(cuda, mode):
+    n = cuda.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    for r in _run(min(n, 4), mode, nccl=True, one_gpu=False):
+        assert r["ok"], r["errors"]
+        assert r["has_nccl"] == 1
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+def test_world1_real_nccl_matches_unsharded(P, cuda, mode):
+    torch = cuda
+    from paper_2208_06399_b200.sharded import ShardComm, a2a_layout, unique_id
+
+    pool = P.generate_pool(6, 5, P.GeneratorConfig(dim_choices=(16, 64), hash_size_max=3e4))
+    B = 257
+    wl = P.generate_workload(1, pool, B)
+    task = P.ShardingTask(pool, 1, [1 << 40])
+    plan = P.ShardingPlan([0] * len(pool))
+    with P.EmbeddingShard(pool, B, weight_seed=9) as ref, P.EmbeddingShard(pool, B, weight_seed=9) as sh:
+        ref.load(wl)
+        sh.load(wl)
+        want = ref.step(0.01, 1e-8, want_loss=True)
+        comm = ShardComm(sh, 0, 1, unique_id())
+        comm.setup(a2a_layout(task, plan, B), mode)
+        if not comm.info().has_nccl:
+            pytest.fail("NCCL communicator not created")
+        if mode == 0:  # without NCCL in the exchange the caller opens the handles
+            comm.open([comm.handle()])
+        got = comm.step(0.01, 1e-8, want_loss=True)
+        torch.cuda.synchronize()
+        assert got == pytest.approx(want, rel=1e-12)
+        assert np.array_equal(comm.recv_tensor().cpu().numpy().reshape(B, -1), ref.read_pooled())
+        for t, tab in enumerate(pool):
+            rows = np.arange(tab.hash_size)
+            assert np.array_equal(sh.read_rows(t, rows), ref.read_rows(t, rows)), tab.id
+            assert np.array_equal(sh.read_momentum(t, rows), ref.read_momentum(t, rows)), tab.id
+        comm.close()
+
+
+def test_comm_argument_errors(P, cuda):
+    from paper_2208_06399_b200.sharded import ShardComm, a2a_layout
+
+    pool = P.generate_pool(6, 3, P.GeneratorConfig(dim_choices=(16,), hash_size_max=1e3))
+    with P.EmbeddingShard(pool, 8) as sh:
+        with pytest.raises(P.ConfigError):
+            ShardComm(sh, 2, 2)
+        c = ShardComm(sh, 0, 1)
+        task = P.ShardingTask(pool, 1, [1 << 40])
+        lay = a2a_layout(task, P.ShardingPlan([0, 0, 0]), 8)
+        with pytest.raises(P.ConfigError):  # NCCL exchange without a communicator
+            c.setup(lay, 3)
+        with pytest.raises(P.StateError):
+            c.forward()
+        lay.shard_dims = [lay.shard_dims[0] + 16]
+        with pytest.raises(P.ShapeError):
+            c.setup(lay, 0)
+        c.close()

@@ -77,7 +77,8 @@ def main():
     run(mixed, 300, streams_of(wl, mixed))
     half = [t for t in mixed if t.dim % 8 == 0]
     run(half, 300, streams_of(wl, half), weights="fp16")
-    run(pool, 512, streams_of(P.generate_workload(0, pool, 512), pool), fwd=False)
+    wl1 = P.generate_workload(0, pool, 512)  # keep the workload alive: the streams are views into it
+    run(pool, 512, streams_of(wl1, pool), fwd=False)
     print("sanitize_case ok")
 
 
