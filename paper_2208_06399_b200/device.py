@@ -80,6 +80,11 @@ class EmbeddingShard:
 
     # -- lifecycle ---------------------------------------------------------
     def close(self):
+        # communicators built on this shard (sharded.ShardComm) go first
+        for c in list(getattr(self, "_comms", [])):
+            c = c()
+            if c is not None:
+                c.close()
         if getattr(self, "_h", None) is not None and self._h.value:
             check(lib().as_destroy(self._h))
             self._h = None

@@ -171,6 +171,9 @@ class ShardComm:
         uid = C.create_string_buffer(nccl_id, UNIQUE_ID_BYTES) if nccl_id is not None else None
         check(lib().as_comm_init(shard._h, uid, rank, world, C.byref(h)))
         self._h = h
+        import weakref
+
+        shard._comms = getattr(shard, "_comms", []) + [weakref.ref(self)]
         self._lib, self._check = lib, check
 
     def setup(self, layout: A2ALayout, mode: int = XCHG_PEER) -> None:

@@ -87,7 +87,7 @@ def test_world1_real_nccl_matches_unsharded(P, cuda, mode):
         comm.setup(a2a_layout(task, plan, B), mode)
         if not comm.info().has_nccl:
             pytest.fail("NCCL communicator not created")
-        if mode == 0:  # without NCCL in the exchange the caller opens the handles
+        with pytest.raises(P.StateError):  # with an NCCL comm, setup exchanged and opened the handles
             comm.open([comm.handle()])
         got = comm.step(0.01, 1e-8, want_loss=True)
         torch.cuda.synchronize()
