@@ -200,7 +200,7 @@ def measured_peak_hbm():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 7700.0, "fallback (B200_PROFILING.md)"
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s, an earlier measurement on this pool)"
 
 
 def sources_sha():

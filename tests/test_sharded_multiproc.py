@@ -91,7 +91,9 @@ def test_world1_real_nccl_matches_unsharded(P, cuda, mode):
             comm.open([comm.handle()])
         got = comm.step(0.01, 1e-8, want_loss=True)
         torch.cuda.synchronize()
-        assert got == pytest.approx(want, rel=1e-12)
+        # the loss is a sum of fp32 partials: here over the receive buffer (its own
+        # kernel), there fused into the forward epilogue -- other groupings
+        assert got == pytest.approx(want, rel=1e-6)
         assert np.array_equal(comm.recv_tensor().cpu().numpy().reshape(B, -1), ref.read_pooled())
         for t, tab in enumerate(pool):
             rows = np.arange(tab.hash_size)

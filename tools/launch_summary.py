@@ -11,7 +11,7 @@ import re
 import sys
 from collections import OrderedDict
 
-NOT_STEP = ("init_table_kernel", "at::", "gather_rows_kernel", "row_count_hist")
+NOT_STEP = ("init_table_kernel", "at::", "gather_rows_kernel", "row_count_hist", "probe_gather")
 
 
 def main():

@@ -1,6 +1,6 @@
 #!/bin/bash
 # One measurement pass on a GPU box (run under gpurun): bench lines, launch
-# lists and ncu --set full summaries of the step kernels, tagged $1 (e.g. r1v7).
+# lists and ncu --set full summaries of ONE step's kernels, tagged $1 (e.g. r2v3).
 # The .ncu-rep files stay on the box unless KEEP_REP=1 (gpurun copies back <= 64 MiB).
 tag=${1:-run}
 set -x
@@ -9,13 +9,16 @@ timeout 300 python bench.py > gpurun_out/${tag}_bench_cfg2.json 2> gpurun_out/${
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_bench_ref.json 2>&1
 timeout 300 python bench.py --workload cfg4 --no-cpu > gpurun_out/${tag}_bench_cfg4.json 2> gpurun_out/${tag}_bench_cfg4.err
 timeout 300 python bench.py --workload cfg3 --no-cpu --no-e2e > gpurun_out/${tag}_bench_cfg3.json 2>&1
+# kernels per step: K4 + 3 sort kernels per digit pass (3 passes: tables up to 2^24 rows) + K1 + 3 fixups + K3 + 3 fixups
+N=18
 for w in cfg2 cfg4; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches_$w.csv \
     python bench.py --workload $w --steps 2 --warmup 3 --profile-only > /dev/null 2>&1
   python tools/launch_summary.py gpurun_out/${tag}_launches_$w.csv gpurun_out/${tag}_launches_$w.txt \
     "ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --workload $w --steps 2 --warmup 3 --profile-only" > /dev/null
   rm -f gpurun_out/${tag}_launches_$w.csv
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"seg_reduce|sort_onesweep|bag_expand|sort_hist|fixup_lane" -c 9 \
+  # one whole step (the 4th, after 3 warm-up steps)
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"seg_|sort_|bag_expand" -s $((3 * N)) -c $N \
     -o /tmp/prof_${tag}_$w python bench.py --workload $w --steps 1 --warmup 3 --profile-only > gpurun_out/${tag}_ncu_$w.log 2>&1
   python tools/ncu_summary.py /tmp/prof_${tag}_$w.ncu-rep gpurun_out/${tag}_ncu_full_$w.txt $w > /dev/null 2>&1
   [ "$KEEP_REP" = 1 ] && cp /tmp/prof_${tag}_$w.ncu-rep gpurun_out/

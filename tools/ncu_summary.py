@@ -31,9 +31,13 @@ METRICS = [
     ("smsp__inst_executed.sum", "warp instr"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe %"),
 ]
-PHASE = {"seg_reduce_kernel<1>": "fwd_segreduce", "seg_reduce_kernel<0>": "bwd_segreduce_adagrad",
-         "seg_fixup_lane_kernel<1>": "fwd_fixup", "seg_fixup_lane_kernel<0>": "bwd_fixup",
-         "bag_expand_kernel": "bag_expand"}
+# kernel-name prefix -> bench.py phase (several kernels of one phase in one
+# step, e.g. the sort's upsweep/scan/downsweep of every pass, are summed)
+PHASE = [("seg_reduce_kernel<1", "fwd_segreduce"), ("seg_reduce_kernel<0", "bwd_segreduce_adagrad"),
+         ("seg_fixup_lane_kernel<1", "fwd_fixup"), ("seg_fixup_kernel<1", "fwd_fixup"),
+         ("seg_fixup_long_kernel<1", "fwd_fixup"), ("seg_fixup_lane_kernel<0", "bwd_fixup"),
+         ("seg_fixup_kernel<0", "bwd_fixup"), ("seg_fixup_long_kernel<0", "bwd_fixup"),
+         ("bag_expand_kernel", "bag_expand"), ("sort_", "radix_sort")]
 
 
 def main():
@@ -61,10 +65,14 @@ def main():
         if "dram__bytes_read.sum" in vals:
             tot = tobytes(vals["dram__bytes_read.sum"]) + tobytes(vals["dram__bytes_write.sum"])
             lines.append(f"  {'dram bytes (r+w)':26s} {tot:20.0f} byte")
-            for k, ph in PHASE.items():
-                if k in name:
-                    # first launch of each phase (a capture may hold several steps)
-                    traffic.setdefault(ph, {"dram_bytes_per_launch": tot, "summary": os.path.basename(out)})
+            for k, ph in PHASE:
+                if name.startswith(k) or (" " + k) in name:
+                    # the capture holds exactly one step (tools/measure_round.sh): sum per phase
+                    e = traffic.setdefault(ph, {"dram_bytes_per_launch": 0.0, "kernels": 0,
+                                                "summary": os.path.basename(out)})
+                    e["dram_bytes_per_launch"] += tot
+                    e["kernels"] += 1
+                    break
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out), "ncu_traffic.json")
