@@ -306,9 +306,20 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
                "carveout");
   }
-  cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+  {
+    // the side stream runs K2 beside the forward gather; ASB_SIDE_PRIO (A/B):
+    // -1 = greatest priority (the sort's CTAs are scheduled first), 1 = least
+    int lo = 0, hi = 0, prio = 0;
+    cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    if (const char* e = std::getenv("ASB_SIDE_PRIO")) {
+      const int v = std::atoi(e);
+      prio = v < 0 ? hi : (v > 0 ? lo : 0);
+    }
+    cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, prio), "side stream");
+  }
   cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_k4_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
 
   // K6: weights from the counter hash, momentum zero.
@@ -358,6 +369,7 @@ EmbContext::~EmbContext() {
   }
   if (ev_fork_) cudaEventDestroy(ev_fork_);
   if (ev_join_) cudaEventDestroy(ev_join_);
+  if (ev_k4_) cudaEventDestroy(ev_k4_);
   if (ev_done_) cudaEventDestroy(ev_done_);
   if (h_loss_) cudaFreeHost(h_loss_);
   if (prev >= 0) cudaSetDevice(prev);
@@ -381,13 +393,13 @@ void EmbContext::ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units) {
     tbag_ = static_cast<int*>(dalloc(sizeof(int) * cap));
     cap_L_ = cap;
   }
-  // K2 scratch: [T][4][256] digit bins | [4][T] + [4] tile counters | [4][tiles][256] look-back
-  const int64_t tiles = (L + kSortTile - 1) / kSortTile + T_;
-  if (tiles > cap_sort_tiles_) {
+  // K2 scratch: [superblocks][256] digit counts / output positions of the running pass
+  const int64_t sbs = (L + kSortTile - 1) / kSortTile + T_;  // the smallest superblocks (1 tile)
+  if (sbs > cap_sort_tiles_) {
     cuda_check(cudaDeviceSynchronize(), "grow sync");
     drop(sort_scratch_);
-    const int64_t cap = tiles + tiles / 8 + 16;
-    sort_scratch_ = static_cast<int*>(dalloc(sizeof(int) * (sort_fixed_ints() + kMaxSortPasses * cap * kSortDigits)));
+    const int64_t cap = sbs + sbs / 8 + 16;
+    sort_scratch_ = static_cast<int*>(dalloc(sizeof(int) * cap * kSortDigits));
     cap_sort_tiles_ = cap;
   }
   if (n_chunks > cap_chunks_) {
@@ -517,42 +529,42 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   sl.L = L;
   sl.nch = nch;
   sl.nun = nun;
-  // K2 layout: sort tiles per table, tables taking part in each digit pass
-  // (their tile prefix) and the histogram CTAs
+  // K2 layout: superblocks per table; meta = [superblock -> table] then, per
+  // digit pass, the superblocks of the tables that still have digits left
   {
-    // meta: [hist CTA -> table][hist CTA -> chunk in table][pass p: tile -> table]...
-    int64_t tiles = 0, hctas = 0;
+    // superblock = 1..16 tiles: about 6 waves of 3 CTAs per SM
+    const int64_t want = 148LL * 3 * 6;
+    int sbt = 1;
+    while (sbt < kSortMaxSBTiles && L / ((int64_t)kSortTile * sbt * 2) >= want) sbt *= 2;
+    sl.sort_sb_elems = kSortTile * sbt;
+    const int64_t sbe = sl.sort_sb_elems;
+    int64_t sbs = 0;
     int pmax = 0;
-    std::vector<int64_t> tiles_of(static_cast<size_t>(T_));
+    std::vector<int64_t> sb_of(static_cast<size_t>(T_));
     for (int t = 0; t < T_; ++t) {
       if (n_idx[t] >= (1LL << 30))
         fail(AS_SHAPE, "table " + std::to_string(specs_[t].id) + ": at most 2^30-1 lookups per batch");
-      tiles_of[t] = (n_idx[t] + kSortTile - 1) / kSortTile;
-      sl.tabs[t].sort_tile_off = static_cast<int>(tiles);
-      tiles += tiles_of[t];
-      hctas += (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta;
+      sb_of[t] = (n_idx[t] + sbe - 1) / sbe;
+      sl.tabs[t].sort_tile_off = static_cast<int>(sbs);
+      sbs += sb_of[t];
       if (n_idx[t] > 0) pmax = std::max(pmax, sort_passes_of(sl.tabs[t].sort_bits));
     }
     std::vector<int>& m = sl.sort_meta;
     m.clear();
-    m.reserve(static_cast<size_t>(2 * hctas + pmax * tiles));
-    for (int t = 0; t < T_; ++t)
-      for (int64_t k = 0; k < (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta; ++k) m.push_back(t);
-    for (int t = 0; t < T_; ++t)
-      for (int64_t k = 0; k < (tiles_of[t] + kHistTilesPerCta - 1) / kHistTilesPerCta; ++k) m.push_back((int)k);
+    m.reserve(static_cast<size_t>((1 + pmax) * sbs));
+    for (int t = 0; t < T_; ++t) m.insert(m.end(), static_cast<size_t>(sb_of[t]), t);
     for (int p = 0; p < kMaxSortPasses; ++p) {
       sl.tile_tab_off[p] = static_cast<int64_t>(m.size());
       int64_t acc = 0;
       if (p < pmax)
         for (int t = 0; t < T_; ++t)
           if (n_idx[t] > 0 && sort_passes_of(sl.tabs[t].sort_bits) > p) {
-            m.insert(m.end(), static_cast<size_t>(tiles_of[t]), t);
-            acc += tiles_of[t];
+            for (int64_t k = 0; k < sb_of[t]; ++k) m.push_back(static_cast<int>(sl.tabs[t].sort_tile_off + k));
+            acc += sb_of[t];
           }
       sl.pass_tiles[p] = acc;
     }
-    sl.n_sort_tiles = tiles;
-    sl.n_hist_ctas = hctas;
+    sl.n_sort_tiles = sbs;
     sl.sort_passes = pmax;
   }
   sl.utab.assign(static_cast<size_t>(nun), 0);
@@ -778,7 +790,7 @@ void EmbContext::commit(cudaStream_t s) {
     pass_tiles_[p] = sl.pass_tiles[p];
   }
   n_sort_tiles_ = sl.n_sort_tiles;
-  n_hist_ctas_ = sl.n_hist_ctas;
+  sort_sb_elems_ = sl.sort_sb_elems;
   sort_passes_ = sl.sort_passes;
   idx32_ = sl.d_idx32;
   off32_ = sl.d_off32;
@@ -845,6 +857,8 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
   if (T_ == 0) return;
   float* target = out ? out : out_;
   const long long nb = (long long)T_ * B_;
+  const bool fork = n_chunks_ > 0 && !prof_serial_;
+  if (fork) cuda_check(cudaEventRecord(ev_fork_, s), "fork");
   {
     Phase ph(this, 0, s);
     bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
@@ -853,14 +867,14 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
     ++launches_;
     bag_valid_ = true;
   }
-  if (n_chunks_ == 0) return;
-  if (!prof_serial_) {
-    cuda_check(cudaEventRecord(ev_fork_, s), "fork");
+  if (fork) {
+    cuda_check(cudaEventRecord(ev_k4_, s), "K4 done");
     cuda_check(cudaStreamWaitEvent(side_, ev_fork_, 0), "fork wait");
-    launch_sort(side_);
+    launch_sort(side_, ev_k4_);
     cuda_check(cudaEventRecord(ev_join_, side_), "join");
     sort_pending_ = true;
   }
+  if (n_chunks_ == 0) return;
   SegParams p = seg_params(true);
   p.W_ro = W_;
   p.out = target;
@@ -883,13 +897,13 @@ void EmbContext::forward(float* out, double* loss_dev, cudaStream_t s) {
 }
 
 // K2: stable radix sort of each table's (row, bag) pairs (sort.cuh). Depends
-// only on the loaded batch and the bag ids of K4, so as_forward launches it on
-// a side stream right after K4 where it overlaps the forward gather; the
-// backward joins on it (or sorts inline when no forward ran since the load).
-void EmbContext::launch_sort(cudaStream_t s) {
-  if (!bag_valid_ && T_ > 0) {
-    // no forward since this batch was committed: the sort's values (bag ids)
-    // come from K4 in ids-only mode (no pooled rows written)
+// on the loaded batch and K4's bag ids: as_forward launches it on a side
+// stream at the start of the step, where the pass-0 digit counts overlap K4
+// and the rest overlaps the forward gather (the pass-0 downsweep waits on
+// `k4_done`); the backward joins on it, or sorts inline when no forward ran
+// since the load (K4 then runs in ids-only mode first).
+void EmbContext::launch_sort(cudaStream_t s, cudaEvent_t k4_done) {
+  if (!k4_done && !bag_valid_ && T_ > 0) {
     const long long nb = (long long)T_ * B_;
     bag_expand_kernel<<<grid_for(nb, 32LL * kWarpsPerBlock), kBlock, 0, s>>>(off32_, T_, (int)B_, dtabs_, bag_,
                                                                             nullptr, sum_dim_, PeerOut{});
@@ -902,31 +916,26 @@ void EmbContext::launch_sort(cudaStream_t s) {
   SortParams sp;
   std::memset(&sp, 0, sizeof sp);
   sp.tabs = dtabs_;
-  sp.T = T_;
   sp.keys_in = reinterpret_cast<const unsigned*>(idx32_);
   sp.vals_in = bag_;
   sp.keys_out = reinterpret_cast<unsigned*>(skey_);
   sp.vals_out = sbag_;
   sp.keys_tmp = reinterpret_cast<unsigned*>(tkey_);
   sp.vals_tmp = tbag_;
-  sp.bins = sort_scratch_;
-  sp.ctrs = sp.bins + (int64_t)T_ * kMaxSortPasses * kSortDigits;
-  sp.lookback = sp.ctrs + kMaxSortPasses * T_ + kMaxSortPasses;
-  sp.n_tiles = (int)n_sort_tiles_;
-  sp.hist_tab = sort_meta_;
-  sp.hist_chunk = sort_meta_ + n_hist_ctas_;
-  for (int p = 0; p < kMaxSortPasses; ++p) sp.tile_tab[p] = sort_meta_ + tile_tab_off_[p];
-  const size_t zero = sizeof(int) * (sort_fixed_ints() + (size_t)sort_passes_ * n_sort_tiles_ * kSortDigits);
-  cuda_check(cudaMemsetAsync(sort_scratch_, 0, zero, s), "sort scratch reset");
-  sort_hist_kernel<<<(unsigned)n_hist_ctas_, kHistThreads, 0, s>>>(sp);
-  cuda_check(cudaGetLastError(), "sort_hist_kernel");
-  sort_scan_kernel<<<dim3((unsigned)T_, (unsigned)sort_passes_), kSortDigits, 0, s>>>(sp);
-  cuda_check(cudaGetLastError(), "sort_scan_kernel");
+  sp.hist = sort_scratch_;
+  sp.sb_tab = sort_meta_;
+  sp.sb_elems = sort_sb_elems_;
   for (int p = 0; p < sort_passes_; ++p) {
-    sort_onesweep_kernel<<<(unsigned)pass_tiles_[p], kSortThreads, 0, s>>>(sp, p);
-    cuda_check(cudaGetLastError(), "sort_onesweep_kernel");
+    sp.pass = p;
+    sp.pass_sb = sort_meta_ + tile_tab_off_[p];
+    const unsigned g = static_cast<unsigned>(pass_tiles_[p]);
+    sort_upsweep_kernel<<<g, kSortThreads, 0, s>>>(sp);
+    sort_scan_kernel<<<(unsigned)T_, kSortDigits, 0, s>>>(sp);
+    if (p == 0 && k4_done) cuda_check(cudaStreamWaitEvent(s, k4_done, 0), "wait K4");
+    sort_downsweep_kernel<<<g, kSortThreads, 0, s>>>(sp);
+    cuda_check(cudaGetLastError(), "sort_downsweep_kernel");
   }
-  launches_ += 2 + sort_passes_;
+  launches_ += 3 * sort_passes_;
 }
 
 void EmbContext::backward(const float* grad, float lr, float eps, cudaStream_t s) {
@@ -1182,7 +1191,7 @@ void EmbContext::info(as_ctx_info* o) const {
   o->momentum = M_;
   // bag_expand + seg_reduce/fixup (fwd) + radix sort + seg_reduce/fixup (bwd)
   o->weight_bytes = w_half_ ? 2 : 4;
-  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 9 + 2 + sort_passes_);
+  o->kernels_per_step = T_ == 0 ? 0 : (n_chunks_ == 0 ? 1 : 9 + 3 * sort_passes_);
 }
 
 }  // namespace asb

@@ -65,7 +65,7 @@ class EmbContext {
   void ensure_capacity(int64_t L, int64_t n_chunks, int64_t n_units);
   void* dalloc(size_t bytes);
   SegParams seg_params(bool fwd) const;
-  void launch_sort(cudaStream_t s);
+  void launch_sort(cudaStream_t s, cudaEvent_t k4_done = nullptr);
   template <bool FWD>
   void launch_seg(SegParams p, cudaStream_t s);
 
@@ -81,16 +81,14 @@ class EmbContext {
   int stage_x_ = 32, stage_s_ = 33;
   size_t seg_smem_bytes_ = 0;
   // K2 (sort.cuh): per-batch layout, uploaded at commit
-  int64_t sort_fixed_ints() const {
-    return (int64_t)T_ * kMaxSortPasses * kSortDigits + kMaxSortPasses * (int64_t)T_ + kMaxSortPasses;
-  }
   int* sort_meta_ = nullptr;     // device copy of Slot::sort_meta
   int64_t cap_sort_meta_ = 0;
-  int* sort_scratch_ = nullptr;  // bins | counters | look-back
+  int* sort_scratch_ = nullptr;  // [superblocks][256] digit counts of the running pass
   int64_t cap_sort_tiles_ = 0;
   int64_t tile_tab_off_[kMaxSortPasses] = {0, 0, 0, 0};
   int64_t pass_tiles_[kMaxSortPasses] = {0, 0, 0, 0};
-  int64_t n_sort_tiles_ = 0, n_hist_ctas_ = 0;
+  int64_t n_sort_tiles_ = 0;
+  int sort_sb_elems_ = kSortTile;
   int sort_passes_ = 0;
 
   DevTable* dtabs_ = nullptr;
@@ -115,10 +113,11 @@ class EmbContext {
     std::vector<const int64_t*> src_idx;  // caller's index arrays (error value lookup)
     std::vector<cudaEvent_t> raw_ev;       // per raw piece: its H2D landed
     cudaEvent_t narrowed = nullptr;        // every GPU-narrowed piece done
-    std::vector<int> sort_meta;  // hist CTA -> table | hist CTA -> chunk | per pass: tile -> table
+    std::vector<int> sort_meta;  // superblock -> table | per pass: its superblocks
     int64_t tile_tab_off[kMaxSortPasses] = {0, 0, 0, 0};
     int64_t pass_tiles[kMaxSortPasses] = {0, 0, 0, 0};
-    int64_t n_sort_tiles = 0, n_hist_ctas = 0;
+    int64_t n_sort_tiles = 0;
+    int sort_sb_elems = kSortTile;
     int sort_passes = 0;
     cudaEvent_t copied = nullptr;   // all H2D of the batch landed
     cudaEvent_t retired = nullptr;  // the device no longer reads the batch
@@ -158,7 +157,6 @@ class EmbContext {
   unsigned fixup_lane_grid_ = 592;
   int64_t cap_units_ = 0;
   int64_t n_units_ = 0;
-  bool bag_valid_ = false;  // bag_ holds the current batch's bag ids (K4 ran since the commit)
   PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
   int raw_eighths_ = 0;  // ASB_RAW_EIGHTHS: eighths of the index pieces narrowed on the GPU
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
@@ -167,6 +165,8 @@ class EmbContext {
   float* carry_ = nullptr;
 
   cudaStream_t side_ = nullptr;  // K2 sort overlapped with the forward
+  cudaEvent_t ev_k4_ = nullptr;  // K4 of this step done (the sort's pass-0 downsweep waits on it)
+  bool bag_valid_ = false;       // bag_ holds the current batch's bag ids (K4 ran since the commit)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_done_ = nullptr;
   bool sort_pending_ = false;
   int64_t L_ = 0;

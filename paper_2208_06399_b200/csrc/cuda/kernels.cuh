@@ -107,18 +107,46 @@ __device__ __forceinline__ void gather8h(float4& a, float4& b, bool ok, const ch
 __device__ __forceinline__ float4 ldg_h4(const char* p) {
   return half4_to_float4(__ldg(reinterpret_cast<const uint2*>(p)));
 }
+#ifdef ASB_L2HINTS
+// backward epilogue rows (read once, written once per step): evict-first in L2
+// so they do not push the gradient slabs of the tables in flight out
+__device__ __forceinline__ float4 ld4_evict_first(const float* p) {
+  float4 v;
+  asm volatile(
+      "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n}\n"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4_evict_first(float* p, float4 v) {
+  asm volatile(
+      "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, pol;\n}\n" ::"l"(p),
+      "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+      : "memory");
+}
+#endif
 // Row slice of W (cv-th float4 of row `seg`) in either storage type.
 __device__ __forceinline__ float4 load_w4(const SegParams& p, const DevTable& tb, int seg, int cv) {
   const long long e = tb.w_base + (long long)seg * tb.dim + cv * 4;
   if (p.w_half) return half4_to_float4(*reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(p.W) + e));
+#ifdef ASB_L2HINTS
+  return ld4_evict_first(p.W + e);
+#else
   return *reinterpret_cast<const float4*>(p.W + e);
+#endif
 }
 __device__ __forceinline__ void store_w4(const SegParams& p, const DevTable& tb, int seg, int cv, float4 x) {
   const long long e = tb.w_base + (long long)seg * tb.dim + cv * 4;
   if (p.w_half)
     *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.W) + e) = float4_to_half4(x);
   else
+#ifdef ASB_L2HINTS
+    st4_evict_first(p.W + e, x);
+#else
     *reinterpret_cast<float4*>(p.W + e) = x;
+#endif
 }
 
 // L2 eviction priorities (ASB_L2HINTS): gathered rows (re-read ~L/U times)
@@ -253,9 +281,11 @@ __device__ __forceinline__ void adagrad_row(const SegParams& p, const DevTable& 
 // Predicated variant for lane groups that run converged (GL < 32): every lane
 // of the warp executes it (the group reduction needs them), `active` selects
 // the groups whose segment ends here.
+// `pre`: the row's state was prefetched into wp / mp (with the batch's gathers).
 template <int GL, int NV>
 __device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTable& tb, int seg, const float4 (&g)[NV],
-                                                 int c, bool active) {
+                                                 int c, bool active, bool pre = false,
+                                                 const float4 (*wp)[NV] = nullptr, float mp = 0.f) {
   const int nvec = tb.dim >> 2;
   float sq = 0.f;
 #pragma unroll
@@ -265,7 +295,13 @@ __device__ __forceinline__ void adagrad_row_pred(const SegParams& p, const DevTa
   if (active) {
     float4 w[NV];
     float m_old;
-    load_row_state<GL, NV>(p, tb, seg, c, w, m_old);
+    if (pre) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) w[q] = (*wp)[q];
+      m_old = mp;
+    } else {
+      load_row_state<GL, NV>(p, tb, seg, c, w, m_old);
+    }
     const float m = m_old + sq / (float)tb.dim;
     const float mult = p.lr / (sqrtf(m) + p.eps);
 #pragma unroll
@@ -340,6 +376,9 @@ __device__ __forceinline__ void cp_async_wait() {
 #ifndef ASB_GATHER_U
 #define ASB_GATHER_U 4
 #endif
+#ifndef ASB_GATHER_U_NARROW
+#define ASB_GATHER_U_NARROW 4
+#endif
 constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
 
 // Staged ints per warp and buffer for lane layout `kind`: row ids R*SR, keys R*(SR+1).
@@ -363,7 +402,9 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   constexpr int R = 32 / GL;                       // chunks (groups) per warp
   constexpr int SR = (8 * GL < 32) ? 8 * GL : 32;  // elements per group per super-round
   constexpr int Q = SR / GL;                       // elements staged per lane per super-round
-  constexpr int U = NV >= ASB_GATHER_U ? 1 : ASB_GATHER_U / NV;  // gathers in flight per lane
+  // gathers in flight per lane (narrow rows: more, their warps walk several chunks)
+  constexpr int UG = GL < 32 ? ASB_GATHER_U_NARROW : ASB_GATHER_U;
+  constexpr int U = NV >= UG ? 1 : UG / NV;
   const int lane = threadIdx.x & 31;
   const int g = lane / GL;
   const int c = lane % GL;
@@ -495,7 +536,21 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
       }
       if constexpr (GL < 32) {
         // several chunks per warp: stay converged, handle each element's
-        // segment end with a warp-uniform test and predicated epilogues
+        // segment end with a warp-uniform test and predicated epilogues.
+        // Backward: each group prefetches the row state of the first segment
+        // ending in its batch (issued after the batch's gathers, so both
+        // latencies overlap).
+        float4 wpre[FWD ? 1 : NV];
+        float mpre = 0.f;
+        int spre = -7;
+#ifndef ASB_NO_NARROW_PREFETCH
+        if constexpr (!FWD) {
+          if (ebits) {
+            spre = gs[m0 + __ffs(ebits) - 1];
+            if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
+          }
+        }
+#endif
 #pragma unroll
         for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -511,7 +566,8 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
             if constexpr (FWD) {
               if (endu && !split) store_pooled<GL, NV, PAIR, EXACT>(p, tb, s, acc, c, loss_acc);
             } else {
-              adagrad_row_pred<GL, NV>(p, tb, s, acc, c, endu && !split);
+              if constexpr (!FWD)
+                adagrad_row_pred<GL, NV>(p, tb, s, acc, c, endu && !split, s == spre, &wpre, mpre);
             }
             if (endu) {
 #pragma unroll

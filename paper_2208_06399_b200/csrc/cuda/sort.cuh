@@ -1,137 +1,258 @@
 // K2: stable LSD radix sort of (table-local row, bag) pairs, SEGMENTED BY
-// TABLE. The lookups of a shard are table-major already, and row ids are
-// table-local (< hash_t), so every table is sorted in its own element range
-// with only ceil(bits(hash_t - 1) / 8) digit passes: a 10^4-row table needs
-// 2 passes, a 10^7-row table 3, where one global sort over the shard's
-// concatenated row space (log2(sum hash) = 26..30 bits) needs 4 for every
-// table (pool856: 2.62 passes per lookup on average instead of 4).
+// TABLE, hand-written for sm_100a (no library code).
 //
-// Per pass, every tile (kSortTile elements of ONE table) runs CUB's onesweep
-// agent (block ranking with warp match-any, decoupled look-back, CCCL 2.8,
-// namespaced asb_cub) against the table's own look-back region, tile counter
-// and digit offsets; our kernels around it: the per-table digit histograms of
-// all passes in one read of the keys, their exclusive scans, and the tile ->
-// table mapping. Ping-pong buffers are picked per table so that its LAST pass
-// writes the output arrays.
+// The lookups of a shard are table-major and row ids are table-local
+// (< hash_t), so every table is sorted in its own element range with only
+// ceil(bits(hash_t - 1) / 8) digit passes: 2 for a 10^4-row table, 3 for
+// 10^7 (pool856: 2.62 passes per lookup instead of the 4 a global sort over
+// the shard's concatenated row space needs).
+//
+// Each pass is reduce-then-scan over SUPERBLOCKS (sb_elems elements of one
+// table: 1..16 tiles, chosen per batch for several waves of CTAs):
+//   upsweep    CTA per superblock: digit counts (per-warp smem histograms)
+//   scan       CTA per table: counts -> each superblock's first output
+//              position per digit (digit-major, superblock-minor), in place
+//   downsweep  CTA per superblock, its tiles in order: warp-stable ranking
+//              (match.any peers + per-warp digit counters), warp -> tile
+//              prefix per digit, scatter to the running per-digit position
+// No CTA waits on another (no look-back chain): every superblock's offsets
+// are known before its downsweep starts.
+//
+// Pass 0 reads the values (bag ids) from K4's bag array; its upsweep and
+// scan need only the row ids, so they overlap K4 and only the pass-0
+// downsweep waits for it.
+//
+// Stability: a warp owns a contiguous run of the tile and ranks its items in
+// element order; warps, tiles and superblocks are ranked in element order.
+// Every table's input is in bag order, so the output is sorted by (row, bag).
+// Ping-pong buffers are picked per table so that its LAST pass writes the
+// output arrays.
 #pragma once
-
-#include <cub/block/block_load.cuh>
-#include <cub/block/block_store.cuh>
-#include <cub/agent/agent_radix_sort_onesweep.cuh>
-#include <cub/block/block_scan.cuh>
 
 #include "types.hpp"
 
-
 namespace asb {
 
-namespace cubns = CUB_NS_QUALIFIER;
-
-constexpr int kHistThreads = 256;
-
-#ifndef ASB_SORT_PARTS
-#define ASB_SORT_PARTS 1
-#endif
-#ifndef ASB_SORT_RANK
-#define ASB_SORT_RANK RADIX_RANK_MATCH_EARLY_COUNTS_ANY
-#endif
-#ifndef ASB_SORT_SCAN
-#define ASB_SORT_SCAN BLOCK_SCAN_RAKING_MEMOIZE
-#endif
-using OnesweepPolicy =
-    cubns::AgentRadixSortOnesweepPolicy<ASB_SORT_THREADS, ASB_SORT_ITEMS, unsigned, ASB_SORT_PARTS,
-                                        cubns::ASB_SORT_RANK, cubns::ASB_SORT_SCAN, cubns::RADIX_SORT_STORE_DIRECT,
-                                        kSortBits>;
-using OnesweepAgent = cubns::detail::radix_sort::AgentRadixSortOnesweep<OnesweepPolicy, false, unsigned, int, int, int>;
-
+static_assert(kSortThreads == kSortDigits, "one thread per digit in the scan / prefix steps");
+constexpr int kSortWarps = kSortThreads / 32;
 
 struct SortParams {
   const DevTable* tabs;
-  int T;
-  const unsigned* keys_in;  // batch order (table-local rows)
-  const int* vals_in;       // bag ids
+  int pass;
+  const unsigned* keys_in;  // idx32 (table-local rows, batch order)
+  const int* vals_in;       // bag ids (K4)
   unsigned* keys_out;       // sorted (final)
   int* vals_out;
   unsigned* keys_tmp;  // ping-pong
   int* vals_tmp;
-  int* bins;      // [T][kMaxSortPasses][256]: digit counts, then (in place) exclusive offsets
-  int* lookback;  // [kMaxSortPasses][n_tiles][256]
-  int* ctrs;      // [kMaxSortPasses][T] per-table tile counters (+ kMaxSortPasses spare)
-  int n_tiles;    // sum over tables of ceil(L_t / kSortTile)
-  // work maps (built on the host per batch): histogram CTA -> (table, chunk of
-  // kHistTilesPerCta tiles in the table); pass p: tile (blockIdx) -> table
-  const int* hist_tab;
-  const int* hist_chunk;
-  const int* tile_tab[kMaxSortPasses];
+  int* hist;           // [n_sb][256]: digit counts of the pass, then the first output position per digit
+  const int* sb_tab;   // superblock -> table
+  const int* pass_sb;  // superblocks of the tables taking part in this pass
+  int sb_elems;        // elements per superblock (a multiple of kSortTile)
 };
 
-// Digit counts of every pass of one table, over kHistTilesPerCta sort tiles.
-// Per-warp private sub-histograms keep Zipf-hot digits from serialising the
-// shared-memory atomics of the whole CTA.
-__global__ void __launch_bounds__(kHistThreads) sort_hist_kernel(SortParams sp) {
-  constexpr int kWarps = kHistThreads / 32;
-  __shared__ int h[kWarps][kMaxSortPasses][kSortDigits];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kWarps * kMaxSortPasses * kSortDigits; i += kHistThreads) (&h[0][0][0])[i] = 0;
-  __syncthreads();
-  const int t = __ldg(sp.hist_tab + blockIdx.x);
-  const DevTable tb = sp.tabs[t];
+struct SortView {
+  const unsigned* kin;
+  const int* vin;
+  unsigned* kout;
+  int* vout;
+};
+__device__ __forceinline__ SortView sort_view(const SortParams& sp, const DevTable& tb) {
   const int np = sort_passes_of(tb.sort_bits);
-  const long long lo = (long long)__ldg(sp.hist_chunk + blockIdx.x) * kHistTilesPerCta * kSortTile;
-  const long long hi = min((long long)tb.n_lookups, lo + (long long)kHistTilesPerCta * kSortTile);
-  const unsigned* keys = sp.keys_in + tb.idx_off;
-  int* hw = &h[warp][0][0];
-  for (long long j = lo + threadIdx.x; j < hi; j += kHistThreads) {
-    const unsigned k = __ldcs(keys + j);
-#pragma unroll
-    for (int p = 0; p < kMaxSortPasses; ++p)
-      if (p < np) atomicAdd(hw + p * kSortDigits + ((k >> (p * kSortBits)) & (kSortDigits - 1)), 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < np * kSortDigits; i += kHistThreads) {
-    int s = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += (&h[w][0][0])[i];
-    if (s) atomicAdd(sp.bins + (long long)t * kMaxSortPasses * kSortDigits + i, s);
-  }
-  (void)lane;
-}
-
-// Exclusive scan of each (table, pass) digit histogram, in place.
-__global__ void __launch_bounds__(kSortDigits) sort_scan_kernel(SortParams sp) {
-  using Scan = cubns::BlockScan<int, kSortDigits>;
-  __shared__ typename Scan::TempStorage tmp;
-  const int t = blockIdx.x, p = blockIdx.y;
-  if (p >= sort_passes_of(sp.tabs[t].sort_bits) || sp.tabs[t].n_lookups == 0) return;
-  int* b = sp.bins + ((long long)t * kMaxSortPasses + p) * kSortDigits;
-  int v = b[threadIdx.x], x;
-  Scan(tmp).ExclusiveSum(v, x);
-  b[threadIdx.x] = x;
-}
-
-// One digit pass over the tiles of every table that still has digits left.
-#ifndef ASB_SORT_MINBLOCKS
-#define ASB_SORT_MINBLOCKS 2
-#endif
-__global__ void __launch_bounds__(ASB_SORT_THREADS, ASB_SORT_MINBLOCKS) sort_onesweep_kernel(SortParams sp, int pass) {
-  __shared__ typename OnesweepAgent::TempStorage s;
-  // the table of this tile; the agent's per-table tile counter orders the
-  // look-back (a tile only waits on tiles of its table that already started)
-  const int t = __ldg(sp.tile_tab[pass] + blockIdx.x);
-  const DevTable& tb = sp.tabs[t];
-  const int np = sort_passes_of(tb.sort_bits);
-  // the table's last pass writes the output buffers
-  const bool to_out = ((np - 1 - pass) & 1) == 0;
-  const unsigned* kin = pass == 0 ? sp.keys_in : (to_out ? sp.keys_tmp : sp.keys_out);
-  const int* vin = pass == 0 ? sp.vals_in : (to_out ? sp.vals_tmp : sp.vals_out);
-  unsigned* kout = to_out ? sp.keys_out : sp.keys_tmp;
-  int* vout = to_out ? sp.vals_out : sp.vals_tmp;
+  const bool to_out = ((np - 1 - sp.pass) & 1) == 0;  // the table's last pass writes the output
+  SortView v;
   const long long o = tb.idx_off;
-  OnesweepAgent agent(s, sp.lookback + ((long long)pass * sp.n_tiles + tb.sort_tile_off) * kSortDigits,
-                      sp.ctrs + pass * sp.T + t, nullptr,
-                      sp.bins + ((long long)t * kMaxSortPasses + pass) * kSortDigits, kout + o, kin + o, vout + o,
-                      vin + o, (int)tb.n_lookups, pass * kSortBits, min(kSortBits, tb.sort_bits - pass * kSortBits));
-  agent.Process();
+  v.kin = (sp.pass == 0 ? sp.keys_in : (to_out ? sp.keys_tmp : sp.keys_out)) + o;
+  v.vin = (sp.pass == 0 ? sp.vals_in : (to_out ? sp.vals_tmp : sp.vals_out)) + o;
+  v.kout = (to_out ? sp.keys_out : sp.keys_tmp) + o;
+  v.vout = (to_out ? sp.vals_out : sp.vals_tmp) + o;
+  return v;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Digit counts of one superblock.
+__global__ void __launch_bounds__(kSortThreads) sort_upsweep_kernel(SortParams sp) {
+  __shared__ int h[kSortWarps][kSortDigits];
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) h[w][threadIdx.x] = 0;
+  const int sb = __ldg(sp.pass_sb + blockIdx.x);
+  const int t = __ldg(sp.sb_tab + sb);
+  const DevTable& tb = sp.tabs[t];
+  const SortView v = sort_view(sp, tb);
+  const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
+  const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
+  const int shift = sp.pass * kSortBits;
+  const unsigned* k = v.kin + lo;
+  __syncthreads();
+  int* hw = h[warp];
+  constexpr int U = 8;
+  for (int j0 = 0; j0 < n; j0 += U * kSortThreads) {
+    unsigned x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * kSortThreads + threadIdx.x;
+      x[u] = j < n ? __ldcs(k + j) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (j0 + u * kSortThreads + (int)threadIdx.x < n) atomicAdd(hw + ((x[u] >> shift) & (kSortDigits - 1)), 1);
+  }
+  __syncthreads();
+  int s = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) s += h[w][threadIdx.x];
+  sp.hist[(long long)sb * kSortDigits + threadIdx.x] = s;
+}
+
+// Per table: counts -> first output position of every (superblock, digit),
+// digit-major then superblock order (table-local positions).
+__global__ void __launch_bounds__(kSortDigits) sort_scan_kernel(SortParams sp) {
+  __shared__ int ws[kSortDigits / 32];
+  const DevTable& tb = sp.tabs[blockIdx.x];
+  if (tb.n_lookups == 0 || sp.pass >= sort_passes_of(tb.sort_bits)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsb = (int)((tb.n_lookups + sp.sb_elems - 1) / sp.sb_elems);
+  int* h = sp.hist + (long long)tb.sort_tile_off * kSortDigits + threadIdx.x;
+  int tot = 0;
+  int k = 0;
+  for (; k + 4 <= nsb; k += 4)
+    tot += h[(long long)k * kSortDigits] + h[(long long)(k + 1) * kSortDigits] + h[(long long)(k + 2) * kSortDigits] +
+           h[(long long)(k + 3) * kSortDigits];
+  for (; k < nsb; ++k) tot += h[(long long)k * kSortDigits];
+  int x = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  int run = x - tot;
+  for (int w = 0; w < warp; ++w) run += ws[w];
+  for (k = 0; k < nsb; ++k) {
+    const int c = h[(long long)k * kSortDigits];
+    h[(long long)k * kSortDigits] = run;
+    run += c;
+  }
+}
+
+#ifndef ASB_SORT_MINBLOCKS
+#define ASB_SORT_MINBLOCKS 3
+#endif
+// Per tile: the keys and values come into registers (warp-striped: a warp
+// owns a contiguous run of the tile), are ranked stably, placed in shared
+// memory in digit order, and written out from there so consecutive threads
+// store consecutive positions of a digit's run (coalesced: the first pass's
+// input is in bag order, so a warp's 32 elements would otherwise hit ~24
+// different sectors). The next tile's loads are issued before this tile's
+// write-out, so their latency overlaps it.
+__global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downsweep_kernel(SortParams sp) {
+  constexpr int I = kSortItems;
+  __shared__ unsigned lkey[kSortTile];            // the tile in digit order
+  __shared__ int lval[kSortTile];
+  __shared__ int cnt[kSortWarps][kSortDigits];     // per-warp digit counts, then per-warp tile offsets
+  __shared__ int gbase[kSortDigits];               // running output position per digit
+  __shared__ int gdelta[kSortDigits];              // output position - tile position, per digit
+  __shared__ int wsum[kSortWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sb = __ldg(sp.pass_sb + blockIdx.x);
+  const int t = __ldg(sp.sb_tab + sb);
+  const DevTable& tb = sp.tabs[t];
+  const SortView v = sort_view(sp, tb);
+  const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
+  const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
+  const int shift = sp.pass * kSortBits;
+  gbase[threadIdx.x] = sp.hist[(long long)sb * kSortDigits + threadIdx.x];
+  const unsigned lt = lanemask_lt();
+  const unsigned* kin = v.kin + lo;
+  const int* vin = v.vin + lo;
+  const int wb = warp * (I * 32);
+  unsigned key[I];
+  int val[I];
+  auto load = [&](int a) {
+    const int nt = min(kSortTile, n - a);
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const int e = wb + i * 32 + lane;
+      key[i] = e < nt ? __ldcs(kin + a + e) : 0u;
+      val[i] = e < nt ? __ldcs(vin + a + e) : 0;
+    }
+  };
+  load(0);
+  for (int a = 0; a < n; a += kSortTile) {
+    const int nt = min(kSortTile, n - a);
+    // warp-stable ranking
+#pragma unroll
+    for (int q = 0; q < kSortDigits / 32; ++q) cnt[warp][q * 32 + lane] = 0;
+    __syncwarp();
+    int rk[I];
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      const bool ok = wb + i * 32 + lane < nt;
+      const unsigned d = ok ? (key[i] >> shift) & (kSortDigits - 1) : kSortDigits + lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int before = __popc(peers & lt);
+      const int c = ok ? cnt[warp][d] : 0;
+      __syncwarp();
+      if (ok && (peers >> lane) == 1u) cnt[warp][d] = c + before + 1;  // highest lane of the group
+      __syncwarp();
+      rk[i] = c + before;
+    }
+    __syncthreads();
+    {
+      // digit d: tile count, exclusive scan over digits (tile offset), warp offsets
+      const int d = threadIdx.x;
+      int c = 0;
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) c += cnt[w][d];
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      int toff = x - c;
+      for (int w = 0; w < warp; ++w) toff += wsum[w];
+      gdelta[d] = gbase[d] - toff;
+      gbase[d] += c;
+      int run = toff;
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) {
+        const int cw = cnt[w][d];
+        cnt[w][d] = run;
+        run += cw;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < I; ++i) {
+      if (wb + i * 32 + lane < nt) {
+        const int lp = cnt[warp][(key[i] >> shift) & (kSortDigits - 1)] + rk[i];
+        lkey[lp] = key[i];
+        lval[lp] = val[i];
+      }
+    }
+    __syncthreads();
+    if (a + kSortTile < n) load(a + kSortTile);  // in flight during the write-out
+#pragma unroll 4
+    for (int i = 0; i < I; ++i) {
+      const int lp = i * kSortThreads + threadIdx.x;
+      if (lp < nt) {
+        const unsigned k = lkey[lp];
+        const int pos = lp + gdelta[(k >> shift) & (kSortDigits - 1)];
+        v.kout[pos] = k;
+        v.vout[pos] = lval[lp];
+      }
+    }
+  }
 }
 
 }  // namespace asb

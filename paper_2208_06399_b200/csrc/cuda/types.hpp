@@ -3,22 +3,22 @@
 
 #include <vector_types.h>
 
-#ifndef ASB_SORT_THREADS
-#define ASB_SORT_THREADS 384
-#endif
 #ifndef ASB_SORT_ITEMS
-#define ASB_SORT_ITEMS 23
+#define ASB_SORT_ITEMS 16
 #endif
 
 namespace asb {
 
-// K2 (sort.cuh): 8-bit digits, onesweep tiles of 384 x 23 elements
+// K2 (sort.cuh): 8-bit digits; tiles of 256 threads x kSortItems elements;
+// superblocks of 1..kSortMaxSBTiles tiles (the unit of the per-pass digit
+// counts; chosen per batch so that there are several waves of CTAs)
 constexpr int kSortBits = 8;
 constexpr int kSortDigits = 1 << kSortBits;
-constexpr int kSortThreads = ASB_SORT_THREADS;
-constexpr int kSortTile = ASB_SORT_THREADS * ASB_SORT_ITEMS;
-constexpr int kMaxSortPasses = 4;    // table-local rows < 2^31
-constexpr int kHistTilesPerCta = 8;  // histogram CTA = 8 consecutive sort tiles of one table
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = ASB_SORT_ITEMS;
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kSortMaxSBTiles = 16;
+constexpr int kMaxSortPasses = 4;  // table-local rows < 2^31
 __host__ __device__ constexpr int sort_passes_of(int bits) { return (bits + kSortBits - 1) / kSortBits; }
 
 // Per-table device descriptor (host-built, see context.cu).
@@ -37,7 +37,7 @@ struct DevTable {
   int table_id;
   int kind;  // lane layout (GL lanes per row, NV float4 per lane), see kind_gl / kind_nv
   int sort_bits;      // bits of the largest table-local row id (K2 passes = ceil(sort_bits / 8))
-  int sort_tile_off;  // first K2 tile of the table (its look-back region)
+  int sort_tile_off;  // first K2 superblock of the table (its digit-count rows)
 };
 
 // Lane layouts: kinds 0..5: GL = 1..32, NV = 1; 6,7,8: GL = 32, NV = 2,4,8;

@@ -555,3 +555,45 @@ def test_backward_without_forward_after_load(P, oracle, cuda):
         sh.backward(torch.from_numpy(grad).cuda(), LR, EPS)
         torch.cuda.synchronize()
         run_bwd_check(oracle, sh, pool, st_b, grad, seed, B)
+
+
+def test_sort_one_to_four_digit_passes(P, oracle, cuda):
+    """K2 over tables needing 1, 2, 3 and 4 digit passes (hash 200 / 3e4 / 3e6 /
+    2e7 rows), tables spanning many superblocks (>= 65,536 lookups each), bags
+    of one lookup (thousands of bags per sort tile: the bag-id marking takes
+    several rounds), long runs of empty bags and a Zipf-hot row: sorted
+    (row, bag) order bit-exact against numpy's stable argsort, then the
+    backward within tolerance."""
+    torch = cuda
+    B = 20000
+    rng = np.random.default_rng(7)
+    hash_sizes = [200, 30000, 3_000_000, 20_000_000, 5000]
+    lens = [
+        rng.integers(0, 8, size=B),                          # short bags, 1 pass
+        np.where(rng.random(B) < 0.6, 0, rng.integers(1, 40, size=B)),  # 60 % empty bags
+        np.ones(B, dtype=np.int64),                          # one lookup per bag
+        rng.integers(0, 12, size=B),
+        np.concatenate([np.zeros(B // 2, dtype=np.int64), rng.integers(0, 30, size=B - B // 2)]),
+    ]
+
+    def rows(t, n):
+        r = rng.zipf(1.3, size=n) % hash_sizes[t]
+        r[::5] = rng.integers(0, hash_sizes[t], size=len(r[::5]))
+        return r.astype(np.int64)
+
+    st = _handmade(B, lens, rows)
+    tables = [P.TableDesc(id=40 + t, dim=d, hash_size=h, pooling_mean=1.0)
+              for t, (h, d) in enumerate(zip(hash_sizes, (16, 32, 64, 128, 8)))]
+    seed = 13
+    grad = grad_grid(3, B, sum(t.dim for t in tables))
+    with P.EmbeddingShard(tables, B, weight_seed=seed) as sh:
+        sh.load(st)
+        sh.backward(torch.from_numpy(grad).cuda(), LR, EPS)
+        torch.cuda.synchronize()
+        row_off = np.cumsum([0] + hash_sizes)[:-1]
+        glob = np.concatenate([i + r0 for (_, i), r0 in zip(st, row_off)]).astype(np.int64)
+        bags = np.concatenate([bag_ids(o) for o, _ in st])
+        order = np.argsort(glob, kind="stable")
+        assert np.array_equal(sh.read_buffer(P.device.SORTED_ROWS).astype(np.int64), glob[order])
+        assert np.array_equal(sh.read_buffer(P.device.SORTED_BAGS), bags[order])
+        run_bwd_check(oracle, sh, tables, st, grad, seed, B)
