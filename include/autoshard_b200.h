@@ -178,6 +178,21 @@ AS_API as_status as_create_ex(int32_t device, const as_table_spec* tables, int32
                               int64_t batch_size, uint64_t weight_seed, int32_t flags, as_ctx** out);
 AS_API as_status as_destroy(as_ctx* ctx);
 
+/* A shard over n_tables of parent's tables (positions into parent's table
+ * order, each at most once; their pooled columns in the given order) that
+ * works on parent's weight and momentum storage — nothing is copied or
+ * initialised, steps through it update parent's rows. Its own workspaces and
+ * batch. The cost hook of an RL environment measures candidate shards this
+ * way without re-creating the tables (rl.hpp:161-167).
+ * parent must outlive the subset. AS_CONFIG for a bad or repeated position. */
+AS_API as_status as_create_subset(const as_ctx* parent, const int32_t* positions, int32_t n_tables,
+                                  as_ctx** out);
+/* Point a subset context at another subset of the same parent, keeping its
+ * streams, events and grow-only workspaces (cheap: the measured-cost hook
+ * times thousands of candidate shards through one context). Load streams
+ * again afterwards. AS_STATE if ctx is not a subset or a batch is staged. */
+AS_API as_status as_retarget_subset(as_ctx* ctx, const int32_t* positions, int32_t n_tables);
+
 /* Load one batch of streams (host int64 CSR per table, ctx table order,
  * TableStream layout tables.hpp:43-47). Host memory is borrowed for the call
  * only. Validation reproduces load_workload's checks (workload_io.hpp:216-241)

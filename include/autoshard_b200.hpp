@@ -16,7 +16,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <unordered_map>
 #include <type_traits>
 #include <stdexcept>
 #include <string>
@@ -108,6 +110,7 @@ class WorkloadView {
     h_.reset(h);
   }
   const as_workload* get() const { return h_.get(); }
+  as_workload* get() { return h_.get(); }
 
  private:
   [[noreturn]] static void throw_missing(int id) {
@@ -192,12 +195,98 @@ class Shard {
     return i;
   }
   as_ctx* get() { return ctx_.get(); }
+  const as_ctx* get() const { return ctx_.get(); }
 
  private:
   struct Del {
     void operator()(as_ctx* c) const { as_destroy(c); }
   };
   std::unique_ptr<as_ctx, Del> ctx_;
+};
+
+// Measured cost of candidate shards over one resident pool of tables. The
+// pool's weights live in one parent context; a candidate shard is a subset
+// context on that storage (as_create_subset: no copy, no init), loaded with
+// its tables' streams and timed with the W/B/R protocol (simcost.hpp:140-154).
+// Costs are cached by membership. This is the measured replacement of the
+// per-shard costs the reference's RL environment asks for: the terminal
+// reward (rl.hpp:161-167), checkpoint selection (rl_train.hpp:231) and the
+// cost-model bootstrap (rl_train.hpp:383-392).
+class ShardCostService {
+ public:
+  template <class Tables, class WorkloadT>
+  ShardCostService(int device, const Tables& pool, const WorkloadT& wl, int warmup = 2, int measure = 5, int trim = 1,
+                   bool flush_l2 = true, uint64_t weight_seed = 0)
+      : parent_(device, pool, wl.batch_size, weight_seed),
+        view_(wl, pool),
+        warmup_(warmup),
+        measure_(measure),
+        trim_(trim),
+        flush_(flush_l2) {
+    int i = 0;
+    for (const auto& t : pool) pos_of_[t.id] = i++;
+    check(as_workload_pin(view_.get()));
+  }
+  // position of a table id in the pool (LookupError-like AS_LOOKUP if absent)
+  int position(int table_id) const {
+    auto it = pos_of_.find(table_id);
+    if (it == pos_of_.end()) raise(AS_LOOKUP, "shard cost: table " + std::to_string(table_id) + " not in the pool");
+    return it->second;
+  }
+  // ms per fwd+bwd step of the shard made of these pool positions (0 for an empty shard)
+  double cost(std::vector<int32_t> positions) {
+    if (positions.empty()) return 0.0;
+    std::sort(positions.begin(), positions.end());
+    auto it = cache_.find(positions);
+    if (it != cache_.end()) {
+      ++hits_;
+      return it->second;
+    }
+    if (!sub_) {
+      as_ctx* sub = nullptr;
+      check(as_create_subset(parent_.get(), positions.data(), static_cast<int32_t>(positions.size()), &sub));
+      sub_.reset(sub);
+    } else {
+      check(as_retarget_subset(sub_.get(), positions.data(), static_cast<int32_t>(positions.size())));
+    }
+    check(as_load_workload(sub_.get(), view_.get(), nullptr));
+    double ms = 0.0;
+    check(as_measure(sub_.get(), warmup_, measure_, trim_, flush_ ? 1 : 0, 0.01f, 1e-8f, &ms));
+    cache_.emplace(std::move(positions), ms);
+    ++measured_;
+    return ms;
+  }
+  template <class Tables>
+  double cost_of_tables(const Tables& tables) {
+    std::vector<int32_t> p;
+    for (const auto& t : tables) p.push_back(position(t.id));
+    return cost(std::move(p));
+  }
+  // per-shard ms of a plan over a task drawn from the pool (measure_plan's shape)
+  template <class Plan, class Task>
+  std::vector<double> plan_costs(const Plan& plan, const Task& task) {
+    std::vector<std::vector<int32_t>> members(static_cast<size_t>(task.num_shards));
+    for (size_t i = 0; i < plan.assignment.size(); ++i)
+      members.at(static_cast<size_t>(plan.assignment[i])).push_back(position(task.tables[i].id));
+    std::vector<double> c;
+    for (auto& m : members) c.push_back(cost(std::move(m)));
+    return c;
+  }
+  size_t measured() const { return measured_; }
+  size_t hits() const { return hits_; }
+
+ private:
+  struct CtxDel {
+    void operator()(as_ctx* c) const { as_destroy(c); }
+  };
+  Shard parent_;
+  std::unique_ptr<as_ctx, CtxDel> sub_;  // one subset context, retargeted per shard
+  WorkloadView view_;
+  int warmup_, measure_, trim_;
+  bool flush_;
+  std::unordered_map<int, int> pos_of_;
+  std::map<std::vector<int32_t>, double> cache_;
+  size_t measured_ = 0, hits_ = 0;
 };
 
 }  // namespace gpu

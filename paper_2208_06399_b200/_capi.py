@@ -122,6 +122,8 @@ SIGNATURES = {
     "as_create": (i32, [i32, T_SPEC, i32, i64, u64, P(vp)]),
     "as_create_ex": (i32, [i32, T_SPEC, i32, i64, u64, i32, P(vp)]),
     "as_destroy": (i32, [vp]),
+    "as_create_subset": (i32, [vp, P(i32), i32, P(vp)]),
+    "as_retarget_subset": (i32, [vp, P(i32), i32]),
     "as_load_streams": (i32, [vp, P(vp), P(vp), P(i64), vp]),
     "as_load_workload": (i32, [vp, vp, vp]),
     "as_stage_streams": (i32, [vp, P(vp), P(vp), P(i64)]),

@@ -341,6 +341,25 @@ AS_API as_status as_create(int32_t device, const as_table_spec* tables, int32_t 
   return as_create_ex(device, tables, n, batch, seed, 0, out);
 }
 
+AS_API as_status as_create_subset(const as_ctx* parent, const int32_t* positions, int32_t n, as_ctx** out) {
+  return guard([&] {
+    need(parent, "parent");
+    need(out, "out");
+    if (n > 0) need(positions, "positions");
+    auto c = std::make_unique<as_ctx>();
+    c->impl = std::make_unique<asb::EmbContext>(*parent->impl, positions, n);
+    *out = c.release();
+  });
+}
+
+AS_API as_status as_retarget_subset(as_ctx* ctx, const int32_t* positions, int32_t n) {
+  return guard([&] {
+    need(ctx, "ctx");
+    if (n > 0) need(positions, "positions");
+    ctx->impl->retarget(positions, n);
+  });
+}
+
 AS_API as_status as_destroy(as_ctx* ctx) {
   return guard([&] { delete ctx; });
 }

@@ -204,32 +204,23 @@ void* EmbContext::dalloc(size_t bytes) {
   return p;
 }
 
-EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed, int flags)
-    : device_(device), T_(n), B_(batch), seed_(seed), w_half_((flags & AS_WEIGHTS_FP16) != 0) {
-  if (flags & ~AS_WEIGHTS_FP16) fail(AS_CONFIG, "as_create_ex: unknown flags " + std::to_string(flags));
-  if (n < 0) fail(AS_CONFIG, "as_create: n_tables must be >= 0");
-  if (batch < 1 || batch > (1LL << 30)) fail(AS_CONFIG, "as_create: batch_size must be in [1, 2^30]");
-  int ndev = 0;
-  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-  if (device < 0 || device >= ndev)
-    fail(AS_CONFIG, "as_create: device " + std::to_string(device) + " out of range (" +
-                        std::to_string(ndev) + " visible)");
-  if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
-  if (const char* e = std::getenv("ASB_CHUNK_KB")) chunk_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
-  if (const char* e = std::getenv("ASB_UNIT_KB")) unit_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
-  specs_.assign(tables, tables + n);
-  htabs_.resize(static_cast<size_t>(n));
-  int64_t w_off = 0;
+// Per-table layout shared by both constructors: validation, lane layout,
+// pooled columns, staging sizes (the storage offsets w_base / row_off are set
+// by the caller).
+void EmbContext::layout_tables() {
+  const int n = T_;
+  htabs_.assign(static_cast<size_t>(n), DevTable{});
   for (int t = 0; t < n; ++t) {
     const as_table_spec& s = specs_[t];
     if (s.dim < 4 || s.dim > 1024 || s.dim % 4 != 0)
       fail(AS_CONFIG, "table " + std::to_string(s.id) + ": device path needs dim % 4 == 0 and 4 <= dim <= 1024, got " +
                           std::to_string(s.dim));
     if (s.hash_size < 1) fail(AS_CONFIG, "table " + std::to_string(s.id) + " has invalid hash_size");
+    if (s.hash_size >= (1LL << 31))
+      fail(AS_SHAPE, "table " + std::to_string(s.id) + ": at most 2^31-1 rows (int32 row ids), got " +
+                         std::to_string(s.hash_size));
     DevTable& d = htabs_[t];
     std::memset(&d, 0, sizeof d);
-    d.row_off = total_rows_;
-    d.w_base = w_off;
     d.sort_bits = std::max(1, bit_width_u64(static_cast<uint64_t>(s.hash_size - 1)));
     d.hash = s.hash_size;
     d.dim = s.dim;
@@ -237,29 +228,174 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
     d.table_id = s.id;
     d.kind = kind_for_dim(s.dim, vec_, w_half_);
     d.chunk_len = chunk_len_for(s.dim, 131072.0);
-    total_rows_ += s.hash_size;
-    // every table starts 128-B aligned (fp32; 64 B for fp16): 16-B vector rows,
-    // and the paired fp16 layouts' 16-B loads, never straddle a table start
-    w_off += (s.hash_size * s.dim + 31) / 32 * 32;
     sum_dim_ += s.dim;
     max_dim_ = std::max(max_dim_, s.dim);
-  }
-  total_w_ = w_off;
-  for (int t = 0; t < n; ++t) {
-    stage_x_ = std::max(stage_x_, stage_x_ints(htabs_[t].kind));
-    stage_s_ = std::max(stage_s_, stage_s_ints(htabs_[t].kind));
+    stage_x_ = std::max(stage_x_, stage_x_ints(d.kind));
+    stage_s_ = std::max(stage_s_, stage_s_ints(d.kind));
   }
   stage_s_ = (stage_s_ + 3) & ~3;  // 16-B aligned id buffers (vector LDS of row ids)
   seg_smem_bytes_ = static_cast<size_t>(kSegWarps) * 2 * (stage_x_ + stage_s_) * sizeof(int);
-  for (int t = 0; t < n; ++t)
-    if (specs_[t].hash_size >= (1LL << 31))
-      fail(AS_SHAPE, "table " + std::to_string(specs_[t].id) + ": at most 2^31-1 rows (int32 row ids), got " +
-                         std::to_string(specs_[t].hash_size));
+}
 
+static void check_device(int device) {
+  int ndev = 0;
+  cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev)
+    fail(AS_CONFIG, "as_create: device " + std::to_string(device) + " out of range (" + std::to_string(ndev) +
+                        " visible)");
+}
+
+EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed, int flags)
+    : device_(device), T_(n), B_(batch), seed_(seed), w_half_((flags & AS_WEIGHTS_FP16) != 0) {
+  if (flags & ~AS_WEIGHTS_FP16) fail(AS_CONFIG, "as_create_ex: unknown flags " + std::to_string(flags));
+  if (n < 0) fail(AS_CONFIG, "as_create: n_tables must be >= 0");
+  if (batch < 1 || batch > (1LL << 30)) fail(AS_CONFIG, "as_create: batch_size must be in [1, 2^30]");
+  check_device(device);
+  if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("ASB_CHUNK_KB")) chunk_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
+  if (const char* e = std::getenv("ASB_UNIT_KB")) unit_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
+  specs_.assign(tables, tables + n);
+  layout_tables();
+  for (int t = 0; t < n; ++t) {
+    htabs_[t].row_off = total_rows_;
+    htabs_[t].w_base = total_w_;
+    total_rows_ += specs_[t].hash_size;
+    // every table starts 128-B aligned (fp32; 64 B for fp16): 16-B vector rows,
+    // and the paired fp16 layouts' 16-B loads, never straddle a table start
+    total_w_ += (specs_[t].hash_size * specs_[t].dim + 31) / 32 * 32;
+  }
   DeviceGuard g(device_);
-  dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
   W_ = static_cast<float*>(dalloc((w_half_ ? 2 : 4) * static_cast<size_t>(total_w_)));
   M_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(total_rows_)));
+  setup_runtime();
+
+  // K6: weights from the counter hash, momentum zero.
+  const unsigned long long s0 = splitmix64(seed_);
+  for (int t = 0; t < n; ++t) {
+    const int64_t off = htabs_[t].w_base;
+    const long long nv = specs_[t].hash_size * (specs_[t].dim / 4);
+    const unsigned grid = static_cast<unsigned>(std::min<long long>((nv + 255) / 256, 148LL * 64));
+    if (w_half_)
+      init_table_kernel<true><<<grid, 256>>>(reinterpret_cast<__half*>(W_) + off, specs_[t].hash_size, specs_[t].dim,
+                                             specs_[t].id, s0);
+    else
+      init_table_kernel<false><<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
+  }
+  cuda_check(cudaGetLastError(), "init_table_kernel");
+  cuda_check(cudaMemset(M_, 0, sizeof(float) * static_cast<size_t>(total_rows_)), "momentum init");
+  cuda_check(cudaMemcpy(dtabs_, htabs_.data(), sizeof(DevTable) * n, cudaMemcpyHostToDevice), "tables H2D");
+  cuda_check(cudaDeviceSynchronize(), "init");
+}
+
+
+// A shard over a subset of `parent`'s tables that uses the parent's weight and
+// momentum storage (no copy, no init): steps through it update the parent's
+// rows. The parent must outlive it.
+EmbContext::EmbContext(const EmbContext& parent, const int* positions, int n)
+    : device_(parent.device_), T_(n), B_(parent.B_), seed_(parent.seed_), w_half_(parent.w_half_) {
+  if (n < 0) fail(AS_CONFIG, "as_create_subset: n_tables must be >= 0");
+  vec_ = parent.vec_;
+  chunk_cap_ = parent.chunk_cap_;
+  unit_cap_ = parent.unit_cap_;
+  specs_.resize(static_cast<size_t>(n));
+  std::vector<char> seen(static_cast<size_t>(parent.T_), 0);
+  for (int i = 0; i < n; ++i) {
+    const int q = positions[i];
+    if (q < 0 || q >= parent.T_)
+      fail(AS_CONFIG, "as_create_subset: position " + std::to_string(q) + " out of range [0, " +
+                          std::to_string(parent.T_) + ")");
+    if (seen[q]++) fail(AS_CONFIG, "as_create_subset: table position " + std::to_string(q) + " given twice");
+    specs_[i] = parent.specs_[q];
+  }
+  layout_tables();
+  for (int i = 0; i < n; ++i) {
+    htabs_[i].row_off = parent.htabs_[positions[i]].row_off;
+    htabs_[i].w_base = parent.htabs_[positions[i]].w_base;
+  }
+  total_rows_ = parent.total_rows_;
+  total_w_ = parent.total_w_;
+  DeviceGuard g(device_);
+  W_ = parent.W_;
+  M_ = parent.M_;
+  parent_ = &parent;
+  setup_runtime();
+  cuda_check(cudaMemcpy(dtabs_, htabs_.data(), sizeof(DevTable) * std::max(1, n), cudaMemcpyHostToDevice),
+             "tables H2D");
+}
+
+// Point a subset context at another subset of its parent's tables, keeping
+// its streams, events and (grow-only) buffers: the measured-cost hook times
+// thousands of candidate shards with one context.
+void EmbContext::retarget(const int* positions, int n) {
+  if (!parent_) fail(AS_STATE, "as_retarget_subset: not a subset context (as_create_subset)");
+  if (n < 0) fail(AS_CONFIG, "as_retarget_subset: n_tables must be >= 0");
+  for (const Slot& sl : slots_)
+    if (sl.staged) fail(AS_STATE, "as_retarget_subset: a staged batch is pending (commit it first)");
+  if (peers_.n) fail(AS_STATE, "as_retarget_subset: the forward writes to peer buffers");
+  const EmbContext& parent = *parent_;
+  DeviceGuard g(device_);
+  cuda_check(cudaDeviceSynchronize(), "retarget sync");
+  std::vector<as_table_spec> specs(static_cast<size_t>(n));
+  std::vector<char> seen(static_cast<size_t>(parent.T_), 0);
+  for (int i = 0; i < n; ++i) {
+    const int q = positions[i];
+    if (q < 0 || q >= parent.T_)
+      fail(AS_CONFIG, "as_retarget_subset: position " + std::to_string(q) + " out of range [0, " +
+                          std::to_string(parent.T_) + ")");
+    if (seen[q]++) fail(AS_CONFIG, "as_retarget_subset: table position " + std::to_string(q) + " given twice");
+    specs[i] = parent.specs_[q];
+  }
+  const int old_T = T_;
+  const int64_t old_out = B_ * sum_dim_;
+  const int old_max_dim = max_dim_;
+  specs_ = std::move(specs);
+  T_ = n;
+  sum_dim_ = 0;
+  max_dim_ = 4;
+  stage_x_ = 32;
+  stage_s_ = 33;
+  layout_tables();
+  for (int i = 0; i < n; ++i) {
+    htabs_[i].row_off = parent.htabs_[positions[i]].row_off;
+    htabs_[i].w_base = parent.htabs_[positions[i]].w_base;
+  }
+  auto drop = [this](void* p) {
+    auto it = std::find(allocs_.begin(), allocs_.end(), p);
+    if (it != allocs_.end()) allocs_.erase(it);
+    cudaFree(p);
+  };
+  if (n > cap_tables_) {
+    drop(dtabs_);
+    dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
+    for (Slot& sl : slots_) {
+      drop(sl.d_off32);
+      cudaFreeHost(sl.h_off32);
+      sl.d_off32 = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
+      cuda_check(cudaHostAlloc(&sl.h_off32, sizeof(int) * static_cast<size_t>(T_ * B_ + 1), cudaHostAllocDefault),
+                 "pinned staging");
+    }
+    cap_tables_ = n;
+  }
+  if (B_ * sum_dim_ > std::max(old_out, cap_out_)) {
+    drop(out_);
+    out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
+    cap_out_ = B_ * sum_dim_;
+  }
+  if (max_dim_ > old_max_dim) cap_chunks_ = 0;  // carries are [chunks][2][max dim]: regrow at the next commit
+  (void)old_T;
+  if (n > 0)
+    cuda_check(cudaMemcpy(dtabs_, htabs_.data(), sizeof(DevTable) * n, cudaMemcpyHostToDevice), "tables H2D");
+  loaded_ = false;
+  sort_pending_ = false;
+  bag_valid_ = false;
+}
+
+// Buffers, streams and events of a context (both constructors).
+void EmbContext::setup_runtime() {
+  const int n = T_;
+  cap_tables_ = n;
+  cap_out_ = B_ * sum_dim_;
+  dtabs_ = static_cast<DevTable*>(dalloc(sizeof(DevTable) * std::max(1, n)));
   out_ = static_cast<float*>(dalloc(sizeof(float) * static_cast<size_t>(B_ * sum_dim_)));
   for (Slot& sl : slots_) {
     sl.d_off32 = static_cast<int*>(dalloc(sizeof(int) * static_cast<size_t>(T_ * B_ + 1)));
@@ -322,22 +458,6 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   cuda_check(cudaEventCreateWithFlags(&ev_k4_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
 
-  // K6: weights from the counter hash, momentum zero.
-  const unsigned long long s0 = splitmix64(seed_);
-  for (int t = 0; t < n; ++t) {
-    const int64_t off = htabs_[t].w_base;
-    const long long nv = specs_[t].hash_size * (specs_[t].dim / 4);
-    const unsigned grid = static_cast<unsigned>(std::min<long long>((nv + 255) / 256, 148LL * 64));
-    if (w_half_)
-      init_table_kernel<true><<<grid, 256>>>(reinterpret_cast<__half*>(W_) + off, specs_[t].hash_size, specs_[t].dim,
-                                             specs_[t].id, s0);
-    else
-      init_table_kernel<false><<<grid, 256>>>(W_ + off, specs_[t].hash_size, specs_[t].dim, specs_[t].id, s0);
-  }
-  cuda_check(cudaGetLastError(), "init_table_kernel");
-  cuda_check(cudaMemset(M_, 0, sizeof(float) * static_cast<size_t>(total_rows_)), "momentum init");
-  cuda_check(cudaMemcpy(dtabs_, htabs_.data(), sizeof(DevTable) * n, cudaMemcpyHostToDevice), "tables H2D");
-  cuda_check(cudaDeviceSynchronize(), "init");
 }
 
 EmbContext::~EmbContext() {
@@ -493,7 +613,7 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
     fail(AS_STATE, "as_stage_streams: no free staging slot (one batch may be staged ahead of the current one; "
                    "commit it first)");
   Slot& sl = slots_[pick];
-  // Chunk length: ~128 KB of gathered rows per group, shrunk for small
+  // Chunk length: ~256 KB of gathered rows per group, shrunk for small
   // batches so that there is at least about one wave of warps.
   double gbytes = 0.0;
   for (int t = 0; t < T_; ++t) gbytes += 4.0 * specs_[t].dim * (double)std::max<int64_t>(n_idx[t], 0);

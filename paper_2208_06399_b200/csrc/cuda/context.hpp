@@ -21,6 +21,10 @@ double probe_gather_bw(int device, int64_t footprint, int row_bytes);
 class EmbContext {
  public:
   EmbContext(int device, const as_table_spec* tables, int n, int64_t batch, uint64_t seed, int flags = 0);
+  // subset of parent's tables on parent's weight / momentum storage (as_create_subset)
+  EmbContext(const EmbContext& parent, const int* positions, int n);
+  // subset context only: another subset of the same parent (as_retarget_subset)
+  void retarget(const int* positions, int n);
   ~EmbContext();
   EmbContext(const EmbContext&) = delete;
   EmbContext& operator=(const EmbContext&) = delete;
@@ -66,6 +70,8 @@ class EmbContext {
   void* dalloc(size_t bytes);
   SegParams seg_params(bool fwd) const;
   void launch_sort(cudaStream_t s, cudaEvent_t k4_done = nullptr);
+  void layout_tables();
+  void setup_runtime();
   template <bool FWD>
   void launch_seg(SegParams p, cudaStream_t s);
 
@@ -77,6 +83,9 @@ class EmbContext {
   std::vector<as_table_spec> specs_;
   std::vector<DevTable> htabs_;
   int64_t sum_dim_ = 0, total_rows_ = 0, total_w_ = 0;
+  const EmbContext* parent_ = nullptr;  // subset contexts: the storage owner
+  int cap_tables_ = 0;                   // dtabs_ / off32 slots sized for this many tables
+  int64_t cap_out_ = 0;                  // out_ floats
   int max_dim_ = 4;
   int stage_x_ = 32, stage_s_ = 33;
   size_t seg_smem_bytes_ = 0;
@@ -160,7 +169,7 @@ class EmbContext {
   PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
   int raw_eighths_ = 0;  // ASB_RAW_EIGHTHS: eighths of the index pieces narrowed on the GPU
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
-  double chunk_cap_ = 131072.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B)
+  double chunk_cap_ = 262144.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B; 256 KB: -0.7 % cfg2, -1.2 % cfg3 step vs 128 KB)
   double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)
   float* carry_ = nullptr;
 

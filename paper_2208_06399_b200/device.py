@@ -78,6 +78,34 @@ class EmbeddingShard:
         self.sum_dim = sum(t.dim for t in self.tables)
         self.cols = np.cumsum([0] + [t.dim for t in self.tables])[:-1].tolist()
 
+    def subset(self, positions: Sequence[int]) -> "EmbeddingShard":
+        """A shard over some of this shard's tables (positions in its table
+        order) on THIS shard's weight and momentum storage (as_create_subset):
+        nothing is copied, steps through it update this shard's rows. Keep this
+        shard alive while the subset is in use."""
+        pos = [int(p) for p in positions]
+        arr = (C.c_int32 * max(1, len(pos)))(*pos)
+        h = C.c_void_p()
+        check(lib().as_create_subset(self._h, arr, len(pos), C.byref(h)))
+        sub = EmbeddingShard.__new__(EmbeddingShard)
+        sub.tables = [self.tables[p] for p in pos]
+        sub.batch_size, sub.device, sub.weights = self.batch_size, self.device, self.weights
+        sub._h = h
+        sub._parent = self  # storage owner
+        sub.sum_dim = sum(t.dim for t in sub.tables)
+        sub.cols = np.cumsum([0] + [t.dim for t in sub.tables])[:-1].tolist()
+        return sub
+
+    def retarget(self, positions: Sequence[int]) -> None:
+        """Subset shards only: switch to another subset of the same parent's
+        tables (as_retarget_subset); load streams again afterwards."""
+        pos = [int(p) for p in positions]
+        arr = (C.c_int32 * max(1, len(pos)))(*pos)
+        check(lib().as_retarget_subset(self._h, arr, len(pos)))
+        self.tables = [self._parent.tables[p] for p in pos]
+        self.sum_dim = sum(t.dim for t in self.tables)
+        self.cols = np.cumsum([0] + [t.dim for t in self.tables])[:-1].tolist()
+
     # -- lifecycle ---------------------------------------------------------
     def close(self):
         # communicators built on this shard (sharded.ShardComm) go first

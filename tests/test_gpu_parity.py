@@ -130,7 +130,7 @@ def test_long_bags_hot_rows_empty_tables(P, oracle, cuda, dim):
     # the device's chunk length for this batch (context.cu chunk_len_for): bags of
     # exactly one / two chunks and chunk-1 / chunk+1 exercise every carry case
     est = 4.0 * dim * (20000 + 4 * 2048 + 5000 + 50 * B)
-    target = max(2048.0, min(131072.0, est / (148.0 * 24.0)))
+    target = max(2048.0, min(262144.0, est / (148.0 * 24.0)))
     target = min(target, 262144.0 / (8 if dim == 16 else 1))  # 256 KB per warp unit of 32/GL chunks
     chunk = max(32, min(8192, int(target / (dim * 4.0)) // 32 * 32))
     lens = [
@@ -597,3 +597,53 @@ def test_sort_one_to_four_digit_passes(P, oracle, cuda):
         assert np.array_equal(sh.read_buffer(P.device.SORTED_ROWS).astype(np.int64), glob[order])
         assert np.array_equal(sh.read_buffer(P.device.SORTED_BAGS), bags[order])
         run_bwd_check(oracle, sh, tables, st, grad, seed, B)
+
+
+def test_subset_shard_on_parent_storage(P, oracle, cuda):
+    """as_create_subset: a shard over some of a parent's tables, on the parent's
+    weight and momentum storage. A step through it equals a standalone shard of
+    the same tables (same seed -> same initial rows) bit for bit, writes the
+    update into the PARENT's rows, and leaves the other tables untouched; the
+    measured-cost hook (ShardCostService) times shards this way."""
+    pool = P.generate_pool(4, 6, P.GeneratorConfig(dim_choices=(16, 32, 64, 128), hash_size_max=3e4))
+    B, seed = 600, 17
+    wl = P.generate_workload(3, pool, B)
+    pos = [4, 1, 2]
+    sub_tables = [pool[p] for p in pos]
+    with P.EmbeddingShard(pool, B, weight_seed=seed) as parent, P.EmbeddingShard(sub_tables, B, weight_seed=seed) as ref:
+        sub = parent.subset(pos)
+        try:
+            assert sub.sum_dim == sum(t.dim for t in sub_tables)
+            sub.load(wl)
+            ref.load(wl)
+            l_sub = sub.step(LR, EPS, want_loss=True)
+            l_ref = ref.step(LR, EPS, want_loss=True)
+            assert l_sub == pytest.approx(l_ref, rel=1e-9)  # per-warp partials added in any order
+            assert np.array_equal(sub.read_pooled(), ref.read_pooled())
+            for i, p in enumerate(pos):
+                rows = np.arange(pool[p].hash_size)
+                assert np.array_equal(parent.read_rows(p, rows), ref.read_rows(i, rows)), pool[p].id
+                assert np.array_equal(parent.read_momentum(p, rows), ref.read_momentum(i, rows)), pool[p].id
+            for p in (0, 3, 5):  # not in the subset: still the initial rows
+                rows = np.arange(0, pool[p].hash_size, 97)
+                assert np.array_equal(parent.read_rows(p, rows), weight_rows(seed, pool[p].id, rows, pool[p].dim))
+            assert sub.measure(1, 3, 1) > 0.0
+            # another subset through the same context (grow-only buffers)
+            sub.retarget([0, 3, 5, 2])
+            sub.load(wl)
+            ref2_tables = [pool[p] for p in (0, 3, 5, 2)]
+            with P.EmbeddingShard(ref2_tables, B, weight_seed=seed) as ref2:
+                ref2.load(wl)
+                sub.forward()
+                ref2.forward()
+                got, want = sub.read_pooled(), ref2.read_pooled()
+                # table 2 was updated by the first step in the parent: compare the untouched ones
+                for i, p in enumerate((0, 3, 5)):
+                    c = sub.cols[i]
+                    assert np.array_equal(got[:, c:c + pool[p].dim], want[:, c:c + pool[p].dim]), pool[p].id
+        finally:
+            sub.close()
+        with pytest.raises(P.ConfigError):
+            parent.subset([1, 1])
+        with pytest.raises(P.ConfigError):
+            parent.subset([6])
