@@ -349,6 +349,24 @@ AS_API as_status as_backward_sharded(as_comm* comm, const float* grad_recv_or_nu
  * as_backward_sharded(grad = recv). */
 AS_API as_status as_step_sharded(as_comm* comm, float lr, float eps, double* loss_out, void* stream);
 
+/* Input-side exchange of the sparse features (KJT all-to-all):
+ * every rank passes ITS mini-batch — the streams of its samples
+ * [row_start[rank], row_start[rank+1]) for ALL n_all tables of the task, host
+ * int64 CSR per table in task order (TableStream layout, offsets over its own
+ * rows) — with the task's tables and owner[t] = the rank holding table t
+ * (plan.assignment). Each rank validates its own mini-batch with
+ * load_workload's checks and messages, the ranks agree on the outcome, the
+ * lengths and int32 indices go to the owners over NCCL (grouped send/recv),
+ * and every owner assembles its tables' streams over the WHOLE batch (sources
+ * in sample order) on the device and loads them into its ctx as
+ * as_load_streams would. Collective; needs as_alltoall_setup (the sample
+ * split) and an NCCL communicator. AS_SHAPE if the ctx's tables are not this
+ * rank's owner[] tables in task order; AS_OFFSET / AS_INDEX name the table
+ * (and, on the other ranks, the failing rank). */
+AS_API as_status as_load_streams_exchanged(as_comm* comm, int32_t n_all, const as_table_spec* all_tables,
+                                           const int32_t* owner, const int64_t* const* local_offsets,
+                                           const int64_t* const* local_indices, void* stream);
+
 typedef struct as_comm_info {
   int32_t rank, world, mode, has_nccl;
   int64_t recv_rows;     /* rows_p of this rank */

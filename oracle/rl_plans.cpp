@@ -80,13 +80,16 @@ inline GpuHook& gpu_hook() {
   static GpuHook h;
   return h;
 }
+// off while a thread applies a checkpoint (shard_with_checkpoint builds a
+// fresh SIM context and ignores the episode's reward)
+inline thread_local bool gpu_hook_off = false;
 inline int32_t gpu_decode(double w) {
   const long long v = std::llround(w);
   const GpuHook& h = gpu_hook();
   return h.svc->position(h.task_ids.at(static_cast<size_t>(v >> 16)).at(static_cast<size_t>(v & 0xffff)));
 }
 inline double gpu_shard_cost_from_marginals(const std::vector<double>& w, const SimParams& p) {
-  if (!gpu_hook().svc) return shard_cost_from_marginals(w, p);
+  if (!gpu_hook().svc || gpu_hook_off) return shard_cost_from_marginals(w, p);
   std::vector<int32_t> pos;
   for (double x : w) pos.push_back(gpu_decode(x));
   std::lock_guard<std::mutex> lk(gpu_hook().mu);
@@ -94,14 +97,14 @@ inline double gpu_shard_cost_from_marginals(const std::vector<double>& w, const 
 }
 inline std::vector<double> gpu_costs_from_marginals(const std::vector<std::vector<double>>& g, const SimParams& p,
                                                     const BenchConfig& b) {
-  if (!gpu_hook().svc) return measure_costs_from_marginals(g, p, b);
+  if (!gpu_hook().svc || gpu_hook_off) return measure_costs_from_marginals(g, p, b);
   std::vector<double> c;
   for (const auto& w : g) c.push_back(gpu_shard_cost_from_marginals(w, p));
   return c;
 }
 inline std::vector<double> gpu_measure_plan(const ShardingPlan& plan, const ShardingTask& task, const Workload& wl,
                                             const SimParams& p, const BenchConfig& b) {
-  if (!gpu_hook().svc) return measure_plan(plan, task, wl, p, b);
+  if (!gpu_hook().svc || gpu_hook_off) return measure_plan(plan, task, wl, p, b);
   std::lock_guard<std::mutex> lk(gpu_hook().mu);
   return gpu_hook().svc->plan_costs(plan, task);
 }
@@ -315,6 +318,9 @@ int main(int argc, char** argv) {
     const auto res = rl::train(train_tasks, test_tasks, norm, mask, sim, batch, fingerprint(pool), cfg, log);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     rl::save_checkpoint_file(o + ".ckpt", res.checkpoint);
+#ifdef ASB_GPU_REWARD
+    gpu_hook_off = true;
+#endif
     const ShardingPlan plan = rl::shard_with_checkpoint(res.checkpoint, ttask, wl);
     std::ofstream os(o + ".assignment");
     for (size_t i = 0; i < plan.assignment.size(); ++i) os << (i ? " " : "") << plan.assignment[i];

@@ -124,6 +124,7 @@ SIGNATURES = {
     "as_destroy": (i32, [vp]),
     "as_create_subset": (i32, [vp, P(i32), i32, P(vp)]),
     "as_retarget_subset": (i32, [vp, P(i32), i32]),
+    "as_load_streams_exchanged": (i32, [vp, i32, T_SPEC, P(i32), P(vp), P(vp), vp]),
     "as_load_streams": (i32, [vp, P(vp), P(vp), P(i64), vp]),
     "as_load_workload": (i32, [vp, vp, vp]),
     "as_stage_streams": (i32, [vp, P(vp), P(vp), P(i64)]),

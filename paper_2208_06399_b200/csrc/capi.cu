@@ -564,6 +564,23 @@ AS_API as_status as_write_table(as_ctx* ctx, int32_t t, const float* w, const fl
   });
 }
 
+AS_API as_status as_load_streams_exchanged(as_comm* comm, int32_t n_all, const as_table_spec* all_tables,
+                                           const int32_t* owner, const int64_t* const* local_offsets,
+                                           const int64_t* const* local_indices, void* stream) {
+  return guard([&] {
+    need(comm, "comm");
+    if (n_all < 0) asb::fail(AS_CONFIG, "as_load_streams_exchanged: n_all must be >= 0");
+    if (n_all > 0) {
+      need(all_tables, "all_tables");
+      need(owner, "owner");
+      need(local_offsets, "local_offsets");
+      need(local_indices, "local_indices");
+    }
+    comm->impl->load_exchanged(n_all, all_tables, owner, local_offsets, local_indices,
+                               static_cast<cudaStream_t>(stream));
+  });
+}
+
 AS_API as_status as_comm_unique_id(void* id) {
   return guard([&] {
     need(id, "unique_id_out");

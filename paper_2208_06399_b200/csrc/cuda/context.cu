@@ -439,7 +439,17 @@ void EmbContext::setup_runtime() {
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     pct),
                "carveout");
-    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
+    // index staging of 1-lane groups can pass the 48 KB default (any subset's kinds)
+    int max_stage = 0;
+    for (int k = 0; k < kNumKinds; ++k) max_stage = std::max(max_stage, stage_x_ints(k) + ((stage_s_ints(k) + 3) & ~3));
+    const int max_dyn = static_cast<int>(kSegWarps * 2 * max_stage * sizeof(int));
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn),
+               "seg smem");
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn),
+               "seg smem");
+    const double need_b = (double)ASB_SEG_MINBLOCKS_BWD * (double)(seg_smem_bytes_ + 1024);
+    const int pct_b = std::min(100, (int)std::ceil(100.0 * need_b / (228.0 * 1024.0)) + 1);
+    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct_b),
                "carveout");
   }
   {
@@ -606,6 +616,15 @@ bool narrow_rows(const int64_t* src, int* dst, int64_t n, int64_t hash, int row0
 
 void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx) {
   DeviceGuard g(device_);
+  Slot& sl = stage_layout(n_idx);
+  stage_fill_host(sl, offsets, indices, n_idx);
+}
+
+// Lay a batch with n_idx[t] lookups per table out in a free slot (chunks,
+// warp units, sort superblocks, grown buffers) and mark it staged; the data
+// itself comes from stage_fill_host (the caller's int64 CSR) or
+// stage_device (device-resident int32 arrays, e.g. after the KJT exchange).
+EmbContext::Slot& EmbContext::stage_layout(const int64_t* n_idx) {
   int pick = -1;
   for (int k = 0; k < 2 && pick < 0; ++k)
     if (!slots_[k].staged && k != cur_slot_) pick = k;
@@ -710,8 +729,14 @@ void EmbContext::stage(const int64_t* const* offsets, const int64_t* const* indi
   cuda_check(cudaEventSynchronize(sl.copied), "slot reuse");
   sl.err_key = ~0ull;
   sl.err_val = 0;
+  sl.raw_used = false;
   sl.staged = true;
   sl.seq = ++stage_seq_;
+  return sl;
+}
+
+void EmbContext::stage_fill_host(Slot& sl, const int64_t* const* offsets, const int64_t* const* indices,
+                                 const int64_t* n_idx) {
   // background job: narrow + validate + H2D, per table piece, on the pool.
   // raw_eighths_/8 of the index pieces of PINNED tables go host->device as
   // int64 and are narrowed + validated on the GPU (narrow_validate_kernel):
@@ -920,6 +945,24 @@ void EmbContext::commit(cudaStream_t s) {
   n_units_ = sl.nun;
   bag_valid_ = false;  // K4 of this batch has not run yet
   loaded_ = true;
+}
+
+// A batch whose int32 rows and rebased offsets are produced ON THE DEVICE:
+// `fill(d_idx32, d_off32, tabs, stream)` enqueues the kernels that write the
+// slot's arrays (table t's rows at tabs[t].idx_off, offsets[t*B + b] global);
+// commit then orders the step after them (the slot's copied event).
+void EmbContext::stage_device(const int64_t* n_idx,
+                              const std::function<void(int*, int*, const DevTable*, cudaStream_t)>& fill) {
+  DeviceGuard g(device_);
+  Slot& sl = stage_layout(n_idx);
+  sl.src_idx.assign(static_cast<size_t>(T_), nullptr);
+  try {
+    fill(sl.d_idx32, sl.d_off32, sl.tabs.data(), copy_);
+    cuda_check(cudaEventRecord(sl.copied, copy_), "copied");
+  } catch (...) {
+    sl.staged = false;
+    throw;
+  }
 }
 
 // Validation now completes at commit; kept for the C-ABI contract.

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <string>
 #include <exception>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -34,6 +35,11 @@ class EmbContext {
   // asynchronous double-buffered loading: stage (H2D on the copy stream),
   // commit (pack + validate on s), check (sync + report errors)
   void stage(const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx);
+  // a batch filled on the device (KJT exchange): layout from n_idx, then fill
+  // enqueues kernels on `stream` writing (d_idx32, d_off32) for the host-built
+  // table layout `tabs` (idx_off per table); commit as usual
+  void stage_device(const int64_t* n_idx,
+                    const std::function<void(int*, int*, const DevTable*, cudaStream_t)>& fill);
   void commit(cudaStream_t s);
   void check();
   void forward(float* out, double* loss_dev, cudaStream_t s);
@@ -62,6 +68,7 @@ class EmbContext {
 
   int device() const { return device_; }
   int n_tables() const { return T_; }
+  int table_id(int t) const { return specs_[t].id; }
   const as_table_spec& spec(int t) const { return specs_[t]; }
 
  private:
@@ -72,6 +79,9 @@ class EmbContext {
   void launch_sort(cudaStream_t s, cudaEvent_t k4_done = nullptr);
   void layout_tables();
   void setup_runtime();
+  struct Slot;
+  Slot& stage_layout(const int64_t* n_idx);
+  void stage_fill_host(Slot& sl, const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx);
   template <bool FWD>
   void launch_seg(SegParams p, cudaStream_t s);
 

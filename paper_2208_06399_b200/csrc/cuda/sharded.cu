@@ -191,6 +191,7 @@ ShardComm::ShardComm(EmbContext* ctx, const void* uid, int rank, int world) : ct
   cuda_check(cudaMalloc(&loss_, sizeof(double)), "cudaMalloc");
   cuda_check(cudaHostAlloc(&h_loss_, sizeof(double), cudaHostAllocDefault), "pinned");
   for (auto& e : ev_) cuda_check(cudaEventCreate(&e), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_kjt_, cudaEventDisableTiming), "event");
 }
 
 ShardComm::~ShardComm() {
@@ -206,8 +207,11 @@ ShardComm::~ShardComm() {
       if (peer_flags_[q]) cudaIpcCloseMemHandle(peer_flags_[q]);
     }
   if (comm_) nccl().CommDestroy(comm_);
-  for (void* p : {(void*)recv_, (void*)grad_, (void*)flags_, (void*)err_, (void*)loss_, (void*)blob_dev_})
+  for (void* p : {(void*)recv_, (void*)grad_, (void*)flags_, (void*)err_, (void*)loss_, (void*)blob_dev_, kjt_meta_,
+                  kjt_send_, kjt_recv_, kjt_geo_, kjt_tabs_})
     if (p) cudaFree(p);
+  if (kjt_h_) cudaFreeHost(kjt_h_);
+  if (ev_kjt_) cudaEventDestroy(ev_kjt_);
   if (h_err_) cudaFreeHost(h_err_);
   if (h_loss_) cudaFreeHost(h_loss_);
   for (auto& e : ev_)
@@ -471,6 +475,282 @@ void ShardComm::profile_read(double* ms2, bool reset) {
   ms2[0] = ms_[0];
   ms2[1] = ms_[1];
   if (reset) ms_[0] = ms_[1] = 0.0;
+}
+
+// ---- input-side exchange of the sparse features (KJT all-to-all) -------------
+// before the forward, every device sends the indices of ITS
+// mini-batch to the owners of the tables. Wire format from rank r to owner q:
+// one int32 block [lengths of q's tables for r's rows, table-major][their
+// indices, table-major]. The owner assembles its tables' streams over the
+// whole batch (sources in rank = sample order) straight into the staging slot
+// of its context: rebased int32 offsets and int32 rows.
+namespace {
+// counts[j * G + r] = sum of source r's lengths of table j
+__global__ void kjt_count_kernel(const int* recv, const long long* src_base, const long long* src_rows, int T, int G,
+                                 long long* counts) {
+  const int j = blockIdx.x, r = blockIdx.y;
+  const int* lens = recv + src_base[r] + (long long)j * src_rows[r];
+  long long sum = 0;
+  for (long long i = threadIdx.x; i < src_rows[r]; i += blockDim.x) sum += lens[i];
+  for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __shared__ long long ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    counts[(long long)j * G + r] = t;
+  }
+}
+struct KjtAssemble {
+  const int* recv;
+  const long long* src_base;  // [G] start of source r's block in recv
+  const long long* src_rows;  // [G] rows of source r
+  const long long* row_start; // [G] first sample of source r
+  const long long* seg;       // [T*G] offset of (j, r)'s indices inside r's index part
+  const long long* dst;       // [T*G] element offset of (j, r) inside table j (sum of earlier sources)
+  const long long* cnt;       // [T*G]
+  const DevTable* tabs;       // slot layout (idx_off)
+  int* idx32;
+  int* off32;
+  int T, G;
+  long long B, L;
+};
+// CTA per (table j, source r): copy the indices, write the rebased offsets of
+// r's rows (exclusive scan of the lengths in 1024-row pieces)
+__global__ void __launch_bounds__(1024) kjt_assemble_kernel(KjtAssemble a) {
+  const int j = blockIdx.x, r = blockIdx.y;
+  const long long k = (long long)j * a.G + r;
+  const long long rows = a.src_rows[r];
+  const int* lens = a.recv + a.src_base[r] + (long long)j * rows;
+  const int* src = a.recv + a.src_base[r] + (long long)a.T * rows + a.seg[k];
+  const long long base = a.tabs[j].idx_off + a.dst[k];
+  int* dst = a.idx32 + base;
+  for (long long i = threadIdx.x; i < a.cnt[k]; i += blockDim.x) dst[i] = src[i];
+  __shared__ long long ws[32];
+  __shared__ long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  int* off = a.off32 + (long long)j * a.B + a.row_start[r];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long i0 = 0; i0 < rows; i0 += blockDim.x) {
+    const long long i = i0 + threadIdx.x;
+    const long long v = i < rows ? lens[i] : 0;
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    long long pre = carry;
+    for (int q = 0; q < w; ++q) pre += ws[q];
+    if (i < rows) off[i] = (int)(base + pre + x - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = pre + x;
+    __syncthreads();
+  }
+  if (j == a.T - 1 && r == a.G - 1 && threadIdx.x == 0) a.off32[(long long)a.T * a.B] = (int)a.L;
+}
+}  // namespace
+
+void ShardComm::load_exchanged(int n_all, const as_table_spec* all, const int32_t* owner,
+                               const int64_t* const* loff, const int64_t* const* lidx, cudaStream_t s) {
+  if (!setup_) fail(AS_STATE, "as_load_streams_exchanged: call as_alltoall_setup first (the sample split)");
+  if (!comm_) fail(AS_STATE, "as_load_streams_exchanged: needs an NCCL communicator (as_comm_init with an id)");
+  const int G = world_;
+  const int64_t rows = rows_;  // this rank's samples
+  // this rank's tables in task order must be the ctx's tables
+  std::vector<int> mine;
+  for (int t = 0; t < n_all; ++t) {
+    if (owner[t] < 0 || owner[t] >= G)
+      fail(AS_CONFIG, "as_load_streams_exchanged: table " + std::to_string(all[t].id) + " has owner " +
+                          std::to_string(owner[t]) + " outside [0, " + std::to_string(G) + ")");
+    if (owner[t] == rank_) mine.push_back(t);
+  }
+  if ((int)mine.size() != ctx_->n_tables())
+    fail(AS_SHAPE, "as_load_streams_exchanged: rank " + std::to_string(rank_) + " owns " + std::to_string(mine.size()) +
+                       " tables, its context has " + std::to_string(ctx_->n_tables()));
+  for (size_t i = 0; i < mine.size(); ++i)
+    if (ctx_->table_id(static_cast<int>(i)) != all[mine[i]].id)
+      fail(AS_SHAPE, "as_load_streams_exchanged: context table " + std::to_string(i) + " is id " +
+                         std::to_string(ctx_->table_id(static_cast<int>(i))) + ", the plan's is " +
+                         std::to_string(all[mine[i]].id));
+  // ---- sender: validate this rank's mini-batch (load_workload's checks and
+  // messages, workload_io.hpp:216-241) and pack one block per owner ----
+  std::string err;
+  as_status err_code = AS_OK;
+  std::vector<int64_t> send_n(G, 0), send_off(G + 1, 0);
+  for (int t = 0; t < n_all && err.empty(); ++t) {
+    const int64_t* o = loff[t];
+    const std::string where = "table " + std::to_string(all[t].id);
+    if (o[0] != 0) err = where + ": offsets must start at 0, got " + std::to_string(o[0]), err_code = AS_OFFSET;
+    for (int64_t q = 1; q <= rows && err.empty(); ++q)
+      if (o[q] < o[q - 1]) err = where + ": offsets must be nondecreasing at entry " + std::to_string(q), err_code = AS_OFFSET;
+    for (int64_t j = 0; j < (err.empty() ? o[rows] : 0); ++j)
+      if (lidx[t][j] < 0 || lidx[t][j] >= all[t].hash_size) {
+        err = where + ": index " + std::to_string(lidx[t][j]) + " out of range [0, " + std::to_string(all[t].hash_size) + ")";
+        err_code = AS_INDEX;
+        break;
+      }
+    if (err.empty()) send_n[owner[t]] += rows + o[rows];
+  }
+  for (int q = 0; q < G; ++q) send_off[q + 1] = send_off[q] + send_n[q];
+  // ---- 1: block sizes and status, all-to-all of one int64 pair per rank pair ----
+  std::vector<long long> meta(2 * G), rmeta(2 * G);
+  for (int q = 0; q < G; ++q) {
+    meta[2 * q] = err.empty() ? send_n[q] : -1;
+    meta[2 * q + 1] = err.empty() ? 0 : err_code;
+  }
+  grow(&kjt_meta_, &kjt_meta_cap_, 4 * G * sizeof(long long));
+  long long* dmeta = static_cast<long long*>(kjt_meta_);
+  cuda_check(cudaMemcpyAsync(dmeta, meta.data(), 2 * G * sizeof(long long), cudaMemcpyHostToDevice, s), "kjt meta H2D");
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < G; ++q) {
+    nccl_check(nccl().Send(dmeta + 2 * q, 2, ncclInt64, q, comm_, s), "ncclSend");
+    nccl_check(nccl().Recv(dmeta + 2 * G + 2 * q, 2, ncclInt64, q, comm_, s), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  cuda_check(cudaMemcpyAsync(rmeta.data(), dmeta + 2 * G, 2 * G * sizeof(long long), cudaMemcpyDeviceToHost, s),
+             "kjt meta D2H");
+  cuda_check(cudaStreamSynchronize(s), "kjt meta");
+  check_async();
+  if (!err.empty()) fail(err_code, "as_load_streams_exchanged: rank " + std::to_string(rank_) + ": " + err);
+  for (int r = 0; r < G; ++r)
+    if (rmeta[2 * r] < 0)
+      fail(static_cast<as_status>(rmeta[2 * r + 1]),
+           "as_load_streams_exchanged: rank " + std::to_string(r) + "'s mini-batch failed validation");
+  // ---- 2: pack (pinned) and exchange the blocks ----
+  std::vector<int64_t> recv_off(G + 1, 0), src_rows(G);
+  for (int r = 0; r < G; ++r) {
+    recv_off[r + 1] = recv_off[r] + rmeta[2 * r];
+    src_rows[r] = start_[r + 1] - start_[r];
+  }
+  grow_host(&kjt_h_, &kjt_h_cap_, std::max<int64_t>(1, send_off[G]) * sizeof(int));
+  int* h = static_cast<int*>(kjt_h_);
+  {
+    std::vector<int64_t> lpos(G), ipos(G);
+    std::vector<int64_t> tq(G, 0);
+    for (int t = 0; t < n_all; ++t) ++tq[owner[t]];
+    for (int q = 0; q < G; ++q) {
+      lpos[q] = send_off[q];
+      ipos[q] = send_off[q] + tq[q] * rows;
+    }
+    for (int t = 0; t < n_all; ++t) {
+      const int q = owner[t];
+      const int64_t* o = loff[t];
+      for (int64_t i = 0; i < rows; ++i) h[lpos[q] + i] = static_cast<int>(o[i + 1] - o[i]);
+      lpos[q] += rows;
+      for (int64_t j = 0; j < o[rows]; ++j) h[ipos[q] + j] = static_cast<int>(lidx[t][j]);
+      ipos[q] += o[rows];
+    }
+  }
+  grow(&kjt_send_, &kjt_send_cap_, std::max<int64_t>(1, send_off[G]) * sizeof(int));
+  grow(&kjt_recv_, &kjt_recv_cap_, std::max<int64_t>(1, recv_off[G]) * sizeof(int));
+  int* dsend = static_cast<int*>(kjt_send_);
+  int* drecv = static_cast<int*>(kjt_recv_);
+  cuda_check(cudaMemcpyAsync(dsend, h, send_off[G] * sizeof(int), cudaMemcpyHostToDevice, s), "kjt H2D");
+  nccl_check(nccl().GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < G; ++q) {
+    if (send_n[q] > 0) nccl_check(nccl().Send(dsend + send_off[q], send_n[q], ncclInt32, q, comm_, s), "ncclSend");
+    if (rmeta[2 * q] > 0) nccl_check(nccl().Recv(drecv + recv_off[q], rmeta[2 * q], ncclInt32, q, comm_, s), "ncclRecv");
+  }
+  nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
+  // ---- 3: per (table, source) counts -> the batch layout on the host ----
+  const int T = ctx_->n_tables();
+  std::vector<long long> geo(4 * G + 3 * (size_t)T * G);  // src_base | src_rows | row_start | cnt... staged below
+  long long* g_base = geo.data();
+  long long* g_rows = g_base + G;
+  long long* g_start = g_rows + G;
+  for (int r = 0; r < G; ++r) {
+    g_base[r] = recv_off[r];
+    g_rows[r] = src_rows[r];
+    g_start[r] = start_[r];
+  }
+  grow(&kjt_geo_, &kjt_geo_cap_, geo.size() * sizeof(long long));
+  long long* dgeo = static_cast<long long*>(kjt_geo_);
+  long long* dcnt = dgeo + 4 * G;
+  cuda_check(cudaMemcpyAsync(dgeo, geo.data(), 3 * G * sizeof(long long), cudaMemcpyHostToDevice, s), "kjt geo H2D");
+  std::vector<long long> cnt((size_t)T * G, 0);
+  if (T > 0) {
+    kjt_count_kernel<<<dim3(T, G), 256, 0, s>>>(drecv, dgeo, dgeo + G, T, G, dcnt);
+    cuda_check(cudaGetLastError(), "kjt_count_kernel");
+    cuda_check(cudaMemcpyAsync(cnt.data(), dcnt, cnt.size() * sizeof(long long), cudaMemcpyDeviceToHost, s), "kjt counts");
+  }
+  cuda_check(cudaStreamSynchronize(s), "kjt exchange");
+  check_async();
+  std::vector<int64_t> n_idx(T, 0);
+  long long* seg = dcnt + (size_t)T * G;
+  std::vector<long long> hseg((size_t)T * G), hdst((size_t)T * G);
+  for (int r = 0; r < G; ++r) {
+    long long acc = 0;
+    for (int j = 0; j < T; ++j) {
+      hseg[(size_t)j * G + r] = acc;
+      acc += cnt[(size_t)j * G + r];
+    }
+  }
+  long long L = 0;
+  for (int j = 0; j < T; ++j) {
+    long long acc = 0;
+    for (int r = 0; r < G; ++r) {
+      hdst[(size_t)j * G + r] = acc;
+      acc += cnt[(size_t)j * G + r];
+    }
+    n_idx[j] = acc;
+    L += acc;
+  }
+  cuda_check(cudaMemcpyAsync(seg, hseg.data(), hseg.size() * sizeof(long long), cudaMemcpyHostToDevice, s), "kjt seg");
+  cuda_check(cudaMemcpyAsync(seg + (size_t)T * G, hdst.data(), hdst.size() * sizeof(long long), cudaMemcpyHostToDevice, s),
+             "kjt dst");
+  cuda_check(cudaEventRecord(ev_kjt_, s), "kjt ready");
+  // ---- 4: assemble into the context's staging slot, commit ----
+  const int64_t B = ctx_->batch();
+  ctx_->stage_device(n_idx.data(), [&](int* idx32, int* off32, const DevTable* tabs, cudaStream_t cs) {
+    cuda_check(cudaStreamWaitEvent(cs, ev_kjt_, 0), "kjt wait");
+    if (T == 0) return;
+    // the slot's host-built layout (idx_off per table) goes with the kernel
+    grow(&kjt_tabs_, &kjt_tabs_cap_, sizeof(DevTable) * T);
+    cuda_check(cudaMemcpyAsync(kjt_tabs_, tabs, sizeof(DevTable) * T, cudaMemcpyHostToDevice, cs), "kjt tabs");
+    KjtAssemble a;
+    a.recv = drecv;
+    a.src_base = dgeo;
+    a.src_rows = dgeo + G;
+    a.row_start = dgeo + 2 * G;
+    a.cnt = dcnt;
+    a.seg = seg;
+    a.dst = seg + (size_t)T * G;
+    a.tabs = static_cast<const DevTable*>(kjt_tabs_);
+    a.idx32 = idx32;
+    a.off32 = off32;
+    a.T = T;
+    a.G = G;
+    a.B = B;
+    a.L = L;
+    kjt_assemble_kernel<<<dim3(T, G), 1024, 0, cs>>>(a);
+    cuda_check(cudaGetLastError(), "kjt_assemble_kernel");
+  });
+  ctx_->commit(s);
+  launches_ += 2;
+}
+
+void ShardComm::grow(void** p, int64_t* cap, int64_t bytes) {
+  if (bytes <= *cap) return;
+  if (*p) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    cudaFree(*p);
+  }
+  *cap = bytes + bytes / 8 + 256;
+  cuda_check(cudaMalloc(p, static_cast<size_t>(*cap)), "cudaMalloc");
+}
+
+void ShardComm::grow_host(void** p, int64_t* cap, int64_t bytes) {
+  if (bytes <= *cap) return;
+  if (*p) {
+    cuda_check(cudaDeviceSynchronize(), "grow sync");
+    cudaFreeHost(*p);
+  }
+  *cap = bytes + bytes / 8 + 256;
+  cuda_check(cudaHostAlloc(p, static_cast<size_t>(*cap), cudaHostAllocDefault), "cudaHostAlloc");
 }
 
 }  // namespace asb

@@ -31,6 +31,9 @@ class ShardComm {
   void backward(const float* grad_recv, float lr, float eps, cudaStream_t s);
   void step(float lr, float eps, double* loss_host, cudaStream_t s);
   void info(as_comm_info* out) const;
+  // KJT all-to-all: this rank's mini-batch of every table -> the owners (as_load_streams_exchanged)
+  void load_exchanged(int n_all, const as_table_spec* all, const int32_t* owner, const int64_t* const* local_offsets,
+                      const int64_t* const* local_indices, cudaStream_t s);
   void profile_read(double* ms2, bool reset);
 
  private:
@@ -39,6 +42,8 @@ class ShardComm {
   void barrier(cudaStream_t s);
   void timed(int which, cudaStream_t s, bool begin);
   void collect();
+  void grow(void** p, int64_t* cap, int64_t bytes);
+  void grow_host(void** p, int64_t* cap, int64_t bytes);
 
   EmbContext* ctx_;
   int rank_, world_;
@@ -64,6 +69,11 @@ class ShardComm {
   bool pending_[2] = {false, false};
   double ms_[2] = {0.0, 0.0};
   int64_t launches_ = 0;
+  // KJT exchange buffers (grow-only)
+  void *kjt_meta_ = nullptr, *kjt_send_ = nullptr, *kjt_recv_ = nullptr, *kjt_geo_ = nullptr, *kjt_tabs_ = nullptr;
+  void* kjt_h_ = nullptr;  // pinned send staging
+  int64_t kjt_meta_cap_ = 0, kjt_send_cap_ = 0, kjt_recv_cap_ = 0, kjt_geo_cap_ = 0, kjt_tabs_cap_ = 0, kjt_h_cap_ = 0;
+  cudaEvent_t ev_kjt_ = nullptr;
 };
 
 }  // namespace asb

@@ -96,6 +96,20 @@ def a2a_layout(task: ShardingTask, plan: ShardingPlan, batch: int) -> A2ALayout:
     return A2ALayout(world, batch, dims, members, cols, row_starts(batch, world))
 
 
+def local_batch(streams, row_start: Sequence[int], rank: int):
+    """Rows [row_start[rank], row_start[rank+1]) of each (offsets, indices) CSR:
+    the mini-batch a rank's data loader holds before the KJT exchange."""
+    import numpy as np
+
+    a, b = int(row_start[rank]), int(row_start[rank + 1])
+    out = []
+    for off, idx in streams:
+        off = np.asarray(off, dtype=np.int64)
+        lo, hi = int(off[a]), int(off[b])
+        out.append((off[a:b + 1] - lo, np.asarray(idx, dtype=np.int64)[lo:hi]))
+    return out
+
+
 def local_tables(task: ShardingTask, plan: ShardingPlan, rank: int) -> List[TableDesc]:
     return [task.tables[i] for i in plan.shard_member_indices(task)[rank]]
 
@@ -191,6 +205,27 @@ class ShardComm:
     def open(self, blobs: Sequence[bytes]) -> None:
         allb = b"".join(bytes(b).ljust(HANDLE_BYTES, b"\0")[:HANDLE_BYTES] for b in blobs)
         self._check(self._lib().as_alltoall_open(self._h, C.create_string_buffer(allb, len(allb))))
+
+    def load_exchanged(self, all_tables: Sequence[TableDesc], owner: Sequence[int], local_streams, stream=None) -> None:
+        """KJT all-to-all (as_load_streams_exchanged): local_streams
+        = this rank's mini-batch, (offsets over its own rows, indices) for EVERY
+        table of the task in task order; owner[t] = rank holding table t. After
+        the call this rank's shard holds its tables' streams of the whole batch."""
+        import numpy as np
+
+        from .device import _stream
+        from .tables import specs_to_c
+
+        st = [(np.ascontiguousarray(o, dtype=np.int64), np.ascontiguousarray(i, dtype=np.int64))
+              for o, i in local_streams]
+        n = len(all_tables)
+        if len(st) != n or len(owner) != n:
+            raise ValueError(f"expected {n} local streams and owners, got {len(st)} / {len(owner)}")
+        po = (C.c_void_p * max(1, n))(*[o.ctypes.data for o, _ in st])
+        pi = (C.c_void_p * max(1, n))(*[i.ctypes.data for _, i in st])
+        ow = (C.c_int32 * max(1, n))(*[int(q) for q in owner])
+        self._check(self._lib().as_load_streams_exchanged(self._h, n, specs_to_c(list(all_tables)), ow, po, pi,
+                                                          _stream(stream)))
 
     def forward(self, stream=None) -> None:
         from .device import _stream

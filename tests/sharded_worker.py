@@ -24,7 +24,7 @@ def main():
     import paper_2208_06399_b200 as P
     from helpers import fp_close, to_oracle_tables, weight_rows
     from oracle import Oracle
-    from paper_2208_06399_b200.sharded import a2a_layout, connect, local_tables, recv_table_rows
+    from paper_2208_06399_b200.sharded import a2a_layout, connect, local_batch, local_tables, recv_table_rows
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     mode, use_nccl = int(os.environ["ASB_MODE"]), os.environ.get("ASB_NCCL") == "1"
@@ -79,6 +79,22 @@ def main():
         # more steps: barrier epochs, buffer reuse across steps
         for _ in range(5):
             comm.step(LR, EPS, want_loss=False)
+        if use_nccl:
+            # KJT all-to-all: every rank holds its samples of ALL tables; after the
+            # exchange its shard must hold exactly its tables' whole-batch streams
+            rows_before = sh.read_buffer(P.device.GLOBAL_ROWS)
+            local = local_batch(st_all, lay.row_start, rank)
+            comm.load_exchanged(pool, plan.assignment, local)
+            sh.forward()
+            torch.cuda.synchronize()
+            if not np.array_equal(sh.read_buffer(P.device.GLOBAL_ROWS), rows_before):
+                out["ok"] = False
+                out["errors"].append("KJT exchange: device rows differ from the direct load")
+            want_bags = np.concatenate([np.repeat(np.arange(B, dtype=np.int32), np.diff(st_all[i][0]))
+                                        for i in plan.shard_member_indices(task)[rank]] or [np.zeros(0, np.int32)])
+            if not np.array_equal(sh.read_buffer(P.device.BAG_IDS), want_bags):
+                out["ok"] = False
+                out["errors"].append("KJT exchange: bag segmentation differs")
         comm.step(LR, EPS, want_loss=True)
         i = comm.info()
         out["bytes_sent_fwd"], out["bytes_sent_bwd"] = int(i.bytes_sent_fwd), int(i.bytes_sent_bwd)

@@ -102,6 +102,46 @@ def test_world1_real_nccl_matches_unsharded(P, cuda, mode):
         comm.close()
 
 
+def test_world1_kjt_exchange_matches_direct_load(P, cuda):
+    """as_load_streams_exchanged through a real 1-rank NCCL communicator: the
+    packed lengths + int32 indices go through ncclSend/Recv, the owner assembles
+    offsets and rows on the device; bit-identical to as_load_streams (rows, bag
+    ids, the forward), a second exchange reuses the buffers, and a bad index of
+    the local mini-batch fails with the load path's message."""
+    torch = cuda
+    from paper_2208_06399_b200.sharded import ShardComm, a2a_layout, local_batch, unique_id
+
+    pool = P.generate_pool(8, 6, P.GeneratorConfig(dim_choices=(16, 64), hash_size_max=3e4, pooling_mean_target=9.0))
+    B = 301
+    wl = P.generate_workload(2, pool, B)
+    st = [(wl.find(t.id).offsets, wl.find(t.id).indices) for t in pool]
+    st[2] = (np.zeros(B + 1, dtype=np.int64), np.zeros(0, dtype=np.int64))  # a table without lookups
+    task = P.ShardingTask(pool, 1, [1 << 40])
+    plan = P.ShardingPlan([0] * len(pool))
+    lay = a2a_layout(task, plan, B)
+    with P.EmbeddingShard(pool, B, weight_seed=4) as ref, P.EmbeddingShard(pool, B, weight_seed=4) as sh:
+        ref.load(st)
+        ref.forward()
+        comm = ShardComm(sh, 0, 1, unique_id())
+        comm.setup(lay, 0)
+        for _ in range(2):
+            comm.load_exchanged(pool, plan.assignment, local_batch(st, lay.row_start, 0))
+            comm.forward()  # the fused exchange: pooled rows land in the receive buffer
+            torch.cuda.synchronize()
+            for what in (P.device.GLOBAL_ROWS, P.device.BAG_IDS):
+                assert np.array_equal(sh.read_buffer(what), ref.read_buffer(what))
+            assert np.array_equal(comm.recv_tensor().cpu().numpy().reshape(B, -1), ref.read_pooled())
+        bad = list(local_batch(st, lay.row_start, 0))
+        idx = bad[4][1].copy()
+        idx[3] = pool[4].hash_size
+        bad[4] = (bad[4][0], idx)
+        with pytest.raises(P.IndexError_, match=f"table {pool[4].id}: index {pool[4].hash_size} out of range"):
+            comm.load_exchanged(pool, plan.assignment, bad)
+        with pytest.raises(P.ShapeError):  # the plan gives this rank 5 tables, its context has 6
+            comm.load_exchanged(pool[:5], [0] * 5, bad[:5])
+        comm.close()
+
+
 def test_comm_argument_errors(P, cuda):
     from paper_2208_06399_b200.sharded import ShardComm, a2a_layout
 

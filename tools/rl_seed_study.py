@@ -133,7 +133,7 @@ def main():
         with open(args.out, "w") as f:
             json.dump(out, f, indent=1)
     for k, v in summary.items():
-        if "mean" in v["max_ms"]:
+        if isinstance(v["max_ms"], dict):
             print(f"{k:14s} max {v['max_ms']['mean']:.3f} +- {v['max_ms']['sd']:.3f} ms  balance "
                   f"{v['balance']['mean']:.3f} +- {v['balance']['sd']:.3f}  vs random "
                   f"{v['speedup_vs_random_mean']['mean']:.3f} +- {v['speedup_vs_random_mean']['sd']:.3f}  "
