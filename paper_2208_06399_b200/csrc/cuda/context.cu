@@ -222,6 +222,11 @@ void EmbContext::layout_tables() {
     DevTable& d = htabs_[t];
     std::memset(&d, 0, sizeof d);
     d.sort_bits = std::max(1, bit_width_u64(static_cast<uint64_t>(s.hash_size - 1)));
+#ifdef ASB_NO_PACKED_SORT
+    d.sort_packed = 0;
+#else
+    d.sort_packed = sort_passes_of(d.sort_bits) >= 2 && d.sort_bits + bag_bits() <= 32 ? 1 : 0;
+#endif
     d.hash = s.hash_size;
     d.dim = s.dim;
     d.col = static_cast<int>(sum_dim_);
@@ -1088,6 +1093,7 @@ void EmbContext::launch_sort(cudaStream_t s, cudaEvent_t k4_done) {
   sp.hist = sort_scratch_;
   sp.sb_tab = sort_meta_;
   sp.sb_elems = sort_sb_elems_;
+  sp.bag_bits = bag_bits();
   for (int p = 0; p < sort_passes_; ++p) {
     sp.pass = p;
     sp.pass_sb = sort_meta_ + tile_tab_off_[p];

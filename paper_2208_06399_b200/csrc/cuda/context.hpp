@@ -69,6 +69,12 @@ class EmbContext {
   int device() const { return device_; }
   int n_tables() const { return T_; }
   int table_id(int t) const { return specs_[t].id; }
+  // bits of the largest bag id (K2's packed keys)
+  int bag_bits() const {
+    int b = 0;
+    while (b < 40 && (B_ - 1) >> b) ++b;
+    return b;
+  }
   const as_table_spec& spec(int t) const { return specs_[t]; }
 
  private:

@@ -49,6 +49,7 @@ struct SortParams {
   const int* sb_tab;   // superblock -> table
   const int* pass_sb;  // superblocks of the tables taking part in this pass
   int sb_elems;        // elements per superblock (a multiple of kSortTile)
+  int bag_bits;        // bits of the largest bag id (packed keys: row << bag_bits | bag)
 };
 
 struct SortView {
@@ -69,6 +70,13 @@ __device__ __forceinline__ SortView sort_view(const SortParams& sp, const DevTab
   return v;
 }
 
+// Digit position of this pass in the keys it reads: packed tables carry
+// (row << bag_bits | bag) after pass 0, whose input is the plain row.
+__device__ __forceinline__ int sort_shift(const SortParams& sp, const DevTable& tb, bool as_read) {
+  const bool packed_in = tb.sort_packed && (sp.pass > 0 || !as_read);
+  return sp.pass * kSortBits + (packed_in ? sp.bag_bits : 0);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -87,7 +95,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_upsweep_kernel(SortParams s
   const SortView v = sort_view(sp, tb);
   const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
   const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
-  const int shift = sp.pass * kSortBits;
+  const int shift = sort_shift(sp, tb, true);
   const unsigned* k = v.kin + lo;
   __syncthreads();
   int* hw = h[warp];
@@ -152,26 +160,26 @@ __global__ void __launch_bounds__(kSortDigits) sort_scan_kernel(SortParams sp) {
 // input is in bag order, so a warp's 32 elements would otherwise hit ~24
 // different sectors). The next tile's loads are issued before this tile's
 // write-out, so their latency overlaps it.
-__global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downsweep_kernel(SortParams sp) {
+// MODE 0: rows + bag ids in and out; packed tables (tb.sort_packed): 1 = pass
+// 0 (rows + bag ids in, packed keys out), 2 = keys alone, 3 = the table's
+// last pass (packed keys in, rows + bag ids out) — half the bytes in between.
+struct SortSmem {
+  unsigned lkey[kSortTile];         // the tile in digit order
+  int lval[kSortTile];
+  int cnt[kSortWarps][kSortDigits];  // per-warp digit counts, then per-warp tile offsets
+  int gbase[kSortDigits];            // running output position per digit
+  int gdelta[kSortDigits];           // output position - tile position, per digit
+  int wsum[kSortWarps];
+};
+
+template <int MODE>
+__device__ __forceinline__ void sort_downsweep_body(const SortParams& sp, SortSmem& sm, const SortView& v, int n,
+                                                    int shift) {
   constexpr int I = kSortItems;
-  __shared__ unsigned lkey[kSortTile];            // the tile in digit order
-  __shared__ int lval[kSortTile];
-  __shared__ int cnt[kSortWarps][kSortDigits];     // per-warp digit counts, then per-warp tile offsets
-  __shared__ int gbase[kSortDigits];               // running output position per digit
-  __shared__ int gdelta[kSortDigits];              // output position - tile position, per digit
-  __shared__ int wsum[kSortWarps];
+  constexpr bool VALS_IN = MODE <= 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sb = __ldg(sp.pass_sb + blockIdx.x);
-  const int t = __ldg(sp.sb_tab + sb);
-  const DevTable& tb = sp.tabs[t];
-  const SortView v = sort_view(sp, tb);
-  const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
-  const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
-  const int shift = sp.pass * kSortBits;
-  gbase[threadIdx.x] = sp.hist[(long long)sb * kSortDigits + threadIdx.x];
+  const int bb = sp.bag_bits;
   const unsigned lt = lanemask_lt();
-  const unsigned* kin = v.kin + lo;
-  const int* vin = v.vin + lo;
   const int wb = warp * (I * 32);
   unsigned key[I];
   int val[I];
@@ -180,8 +188,9 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       const int e = wb + i * 32 + lane;
-      key[i] = e < nt ? __ldcs(kin + a + e) : 0u;
-      val[i] = e < nt ? __ldcs(vin + a + e) : 0;
+      key[i] = e < nt ? __ldcs(v.kin + a + e) : 0u;
+      if constexpr (VALS_IN) val[i] = e < nt ? __ldcs(v.vin + a + e) : 0;
+      if constexpr (MODE == 1) key[i] = (key[i] << bb) | (unsigned)val[i];
     }
   };
   load(0);
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
     const int nt = min(kSortTile, n - a);
     // warp-stable ranking
 #pragma unroll
-    for (int q = 0; q < kSortDigits / 32; ++q) cnt[warp][q * 32 + lane] = 0;
+    for (int q = 0; q < kSortDigits / 32; ++q) sm.cnt[warp][q * 32 + lane] = 0;
     __syncwarp();
     int rk[I];
 #pragma unroll
@@ -198,9 +207,9 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
       const unsigned d = ok ? (key[i] >> shift) & (kSortDigits - 1) : kSortDigits + lane;
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int before = __popc(peers & lt);
-      const int c = ok ? cnt[warp][d] : 0;
+      const int c = ok ? sm.cnt[warp][d] : 0;
       __syncwarp();
-      if (ok && (peers >> lane) == 1u) cnt[warp][d] = c + before + 1;  // highest lane of the group
+      if (ok && (peers >> lane) == 1u) sm.cnt[warp][d] = c + before + 1;  // highest lane of the group
       __syncwarp();
       rk[i] = c + before;
     }
@@ -210,24 +219,24 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
       const int d = threadIdx.x;
       int c = 0;
 #pragma unroll
-      for (int w = 0; w < kSortWarps; ++w) c += cnt[w][d];
+      for (int w = 0; w < kSortWarps; ++w) c += sm.cnt[w][d];
       int x = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
-      if (lane == 31) wsum[warp] = x;
+      if (lane == 31) sm.wsum[warp] = x;
       __syncthreads();
       int toff = x - c;
-      for (int w = 0; w < warp; ++w) toff += wsum[w];
-      gdelta[d] = gbase[d] - toff;
-      gbase[d] += c;
+      for (int w = 0; w < warp; ++w) toff += sm.wsum[w];
+      sm.gdelta[d] = sm.gbase[d] - toff;
+      sm.gbase[d] += c;
       int run = toff;
 #pragma unroll
       for (int w = 0; w < kSortWarps; ++w) {
-        const int cw = cnt[w][d];
-        cnt[w][d] = run;
+        const int cw = sm.cnt[w][d];
+        sm.cnt[w][d] = run;
         run += cw;
       }
     }
@@ -235,9 +244,9 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       if (wb + i * 32 + lane < nt) {
-        const int lp = cnt[warp][(key[i] >> shift) & (kSortDigits - 1)] + rk[i];
-        lkey[lp] = key[i];
-        lval[lp] = val[i];
+        const int lp = sm.cnt[warp][(key[i] >> shift) & (kSortDigits - 1)] + rk[i];
+        sm.lkey[lp] = key[i];
+        if constexpr (MODE == 0) sm.lval[lp] = val[i];
       }
     }
     __syncthreads();
@@ -246,12 +255,41 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
     for (int i = 0; i < I; ++i) {
       const int lp = i * kSortThreads + threadIdx.x;
       if (lp < nt) {
-        const unsigned k = lkey[lp];
-        const int pos = lp + gdelta[(k >> shift) & (kSortDigits - 1)];
-        v.kout[pos] = k;
-        v.vout[pos] = lval[lp];
+        const unsigned k = sm.lkey[lp];
+        const int pos = lp + sm.gdelta[(k >> shift) & (kSortDigits - 1)];
+        if constexpr (MODE == 0) {
+          v.kout[pos] = k;
+          v.vout[pos] = sm.lval[lp];
+        } else if constexpr (MODE == 3) {
+          v.kout[pos] = k >> bb;
+          v.vout[pos] = (int)(k & ((1u << bb) - 1u));
+        } else {
+          v.kout[pos] = k;
+        }
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downsweep_kernel(SortParams sp) {
+  __shared__ SortSmem sm;
+  const int sb = __ldg(sp.pass_sb + blockIdx.x);
+  const int t = __ldg(sp.sb_tab + sb);
+  const DevTable& tb = sp.tabs[t];
+  SortView v = sort_view(sp, tb);
+  const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
+  const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
+  v.kin += lo;
+  v.vin += lo;
+  sm.gbase[threadIdx.x] = sp.hist[(long long)sb * kSortDigits + threadIdx.x];
+  const int shift = sort_shift(sp, tb, false);
+  const int mode =
+      !tb.sort_packed ? 0 : (sp.pass == 0 ? 1 : (sp.pass == sort_passes_of(tb.sort_bits) - 1 ? 3 : 2));
+  switch (mode) {
+    case 0: sort_downsweep_body<0>(sp, sm, v, n, shift); break;
+    case 1: sort_downsweep_body<1>(sp, sm, v, n, shift); break;
+    case 2: sort_downsweep_body<2>(sp, sm, v, n, shift); break;
+    default: sort_downsweep_body<3>(sp, sm, v, n, shift); break;
   }
 }
 

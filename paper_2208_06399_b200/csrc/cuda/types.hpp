@@ -38,6 +38,7 @@ struct DevTable {
   int kind;  // lane layout (GL lanes per row, NV float4 per lane), see kind_gl / kind_nv
   int sort_bits;      // bits of the largest table-local row id (K2 passes = ceil(sort_bits / 8))
   int sort_tile_off;  // first K2 superblock of the table (its digit-count rows)
+  int sort_packed;    // K2 sorts 32-bit (row << bag_bits | bag) keys alone (rows + bag ids fit 32 bits, >= 2 passes)
 };
 
 // Lane layouts: kinds 0..5: GL = 1..32, NV = 1; 6,7,8: GL = 32, NV = 2,4,8;
