@@ -92,6 +92,9 @@ class EmbeddingShard:
         sub.batch_size, sub.device, sub.weights = self.batch_size, self.device, self.weights
         sub._h = h
         sub._parent = self  # storage owner
+        import weakref
+
+        self._subsets = getattr(self, "_subsets", []) + [weakref.ref(sub)]
         sub.sum_dim = sum(t.dim for t in sub.tables)
         sub.cols = np.cumsum([0] + [t.dim for t in sub.tables])[:-1].tolist()
         return sub
@@ -108,8 +111,9 @@ class EmbeddingShard:
 
     # -- lifecycle ---------------------------------------------------------
     def close(self):
-        # communicators built on this shard (sharded.ShardComm) go first
-        for c in list(getattr(self, "_comms", [])):
+        # communicators built on this shard (sharded.ShardComm) and subset
+        # shards on its storage go first
+        for c in list(getattr(self, "_comms", [])) + list(getattr(self, "_subsets", [])):
             c = c()
             if c is not None:
                 c.close()

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Workload for compute-sanitizer (memcheck / racecheck / synccheck) over every
-kernel of the hot path (K1-K4 and the fixups): cfg 1, a long-bag / hot-row /
-empty-table case for narrow and wide rows, fp16 storage, and a backward with no
-forward. Only this library's kernels run (no torch); results are checked
+kernel of the hot path (K1-K4 and the fixups, K2's packed and unpacked
+passes): cfg 1, a long-bag / hot-row / empty-table case for narrow and wide
+rows, fp16 storage, a backward with no forward, and subset contexts on a
+parent's storage. Only this library's kernels run (no torch); results are checked
 against the oracle so the sanitised runs are the correct path.
 
 usage: compute-sanitizer --tool memcheck python tools/sanitize_case.py
@@ -79,6 +80,14 @@ def main():
     run(half, 300, streams_of(wl, half), weights="fp16")
     wl1 = P.generate_workload(0, pool, 512)  # keep the workload alive: the streams are views into it
     run(pool, 512, streams_of(wl1, pool), fwd=False)
+    # subset contexts on a parent's storage, retargeted (the measured-cost hook)
+    with P.EmbeddingShard(mixed, 300, weight_seed=3) as parent:
+        sub = parent.subset([4, 1])
+        for pos in ([4, 1], [0, 2, 5], [3]):
+            sub.retarget(pos)
+            sub.load(wl)
+            sub.step(0.01, 1e-8, want_loss=True)
+        sub.close()
     print("sanitize_case ok")
 
 
