@@ -380,6 +380,11 @@ __device__ __forceinline__ void cp_async_wait() {
 #define ASB_GATHER_U_NARROW 4
 #endif
 constexpr int kSegWarps = 8;  // warps per CTA of the segment kernels
+#ifdef ASB_IDX64
+using EIdx = long long;
+#else
+using EIdx = int;  // element index inside a shard (< 2^31, enforced at staging)
+#endif
 
 // Staged ints per warp and buffer for lane layout `kind`: row ids R*SR, keys R*(SR+1).
 __host__ __device__ constexpr int stage_sr(int kind) { return 8 * kind_gl(kind) < 32 ? 8 * kind_gl(kind) : 32; }
@@ -414,9 +419,10 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const int C = tb.chunk_len;
   const int lchunk = (unit - tb.unit_off) * R + g;
   const int chunk = tb.chunk_off + lchunk;
-  const long long t_lo = tb.idx_off, t_hi = tb.idx_off + tb.n_lookups;
-  const long long j_lo = t_lo + (long long)lchunk * C;
-  const long long j_hi = min(j_lo + (long long)C, t_hi);
+  // element indices of the shard fit 32 bits (stage() rejects >= 2^31 lookups)
+  const EIdx t_lo = (EIdx)tb.idx_off, t_hi = (EIdx)(tb.idx_off + tb.n_lookups);
+  const EIdx j_lo = t_lo + (EIdx)lchunk * C;
+  const EIdx j_hi = min(j_lo + (EIdx)C, t_hi);
   const bool live = j_lo < j_hi;
   const int prev_seg = (live && j_lo > t_lo) ? __ldg(p.seg + j_lo - 1) : -1;
 
@@ -441,13 +447,13 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #endif
 
   // stage the row ids [base, base+SR) and keys [base, base+SR] of one super-round
-  auto stage = [&](long long base, int buf) {
+  auto stage = [&](EIdx base, int buf) {
     int* gx = xs + buf * kStageX + g * SR;
     int* gs = ss + buf * kStageS + g * (SR + 1);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int m = q * GL + c;
-      const long long e = base + m;
+      const EIdx e = base + m;
       if (e < j_hi) cp_async4(gx + m, p.src + e);
       if (e < t_hi)
         cp_async4(gs + m, p.seg + e);
@@ -455,7 +461,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
         gs[m] = -2;
     }
     if (c == 0) {
-      const long long e = base + SR;
+      const EIdx e = base + SR;
       if (e < t_hi)
         cp_async4(gs + SR, p.seg + e);
       else
@@ -477,7 +483,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   int buf = 0;
 #pragma unroll 1
   for (int sr = 0; sr < C; sr += SR, buf ^= 1) {
-    const long long base = j_lo + sr;
+    const EIdx base = j_lo + sr;
     if (base + SR < j_hi)
       stage(base + SR, buf ^ 1);
     else
@@ -486,7 +492,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
     __syncwarp();
     const int* gx = xs + buf * kStageX + g * SR;
     const int* gs = ss + buf * kStageS + g * (SR + 1);
-    const int nval = (int)max(0LL, min((long long)SR, j_hi - base));
+    const int nval = (int)max((EIdx)0, min((EIdx)SR, j_hi - base));
     unsigned endm = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
