@@ -299,6 +299,9 @@ def main():
                     help="N>1 pooled-row exchange: peer memory both ways (fused forward), fused forward + NCCL "
                          "backward, or NCCL both ways")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kjt", action="store_true",
+                    help="N>1: also time e2e with the input-side KJT all-to-all (as_load_streams_exchanged): every "
+                         "rank starts from ITS samples of ALL tables (PAPER.md:169)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
     args = ap.parse_args()
@@ -541,6 +544,39 @@ def main():
                "pipelined": "H2D of batch i+1 overlaps compute of batch i (as_stage_workload / as_commit_staged)",
                "loss_last": loss}
 
+    # ---- e2e with the input-side exchange (opt-in): each rank's loader holds
+    # its samples of EVERY table; the indices reach the table owners through
+    # as_load_streams_exchanged (NCCL), then the sharded step ----
+    e2e_kjt = None
+    if args.kjt and world > 1 and not one_gpu and not args.profile_only:
+        try:
+            from paper_2208_06399_b200.sharded import local_batch
+
+            wl_all = P.generate_workload(0, tables_all, B, zipf)
+            full = [(wl_all.find(t.id).offsets, wl_all.find(t.id).indices) for t in tables_all]
+            local = local_batch(full, lay.row_start, rank)
+            del full, wl_all
+            owner = list(plan.assignment)
+            h2d_k = sum(4 * (len(o) - 1) + 4 * len(i) for o, i in local)
+            for _ in range(2):
+                comm.load_exchanged(tables_all, owner, local, stream=stream)
+                comm.step(LR, EPS, want_loss=True, stream=stream)
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(K):
+                comm.load_exchanged(tables_all, owner, local, stream=stream)
+                loss_k = comm.step(LR, EPS, want_loss=True, stream=stream)
+            barrier()
+            te = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            e2e_kjt = {"value": round(B * K / float(te.item()), 1), "unit": "samples/s",
+                       "h2d_bytes_per_step": int(h2d_k), "d2h_bytes_per_step": 16,
+                       "ms_per_step": round(float(te.item()) * 1e3 / K, 3), "loss_last": loss_k,
+                       "path": "local mini-batch of all tables -> validate, pack, H2D, NCCL grouped send/recv, "
+                               "on-device assembly (as_load_streams_exchanged) -> as_step_sharded; not pipelined"}
+        except Exception as e:  # noqa: BLE001  (reported, never silently replaced)
+            e2e_kjt = {"error": f"{type(e).__name__}: {e}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_only:
         cpu = cpu_baseline_leg(mine, wl, B)
@@ -585,6 +621,7 @@ def main():
             "gpu_launches": int(launches),
             "launches_per_step": launches / K,
             "e2e": e2e,
+            "e2e_kjt": e2e_kjt,
             "cpu_baseline": cpu,
             "clocks": sampler.summary() if sampler else None,
             "step_ms_min_median_max": [round(min(step_ms), 4), round(statistics.median(step_ms), 4),
