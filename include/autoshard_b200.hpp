@@ -211,7 +211,8 @@ class Shard {
 // Costs are cached by membership. This is the measured replacement of the
 // per-shard costs the reference's RL environment asks for: the terminal
 // reward (rl.hpp:161-167), checkpoint selection (rl_train.hpp:231) and the
-// cost-model bootstrap (rl_train.hpp:383-392).
+// cost-model bootstrap (rl_train.hpp:383-392). Not thread-safe: one caller
+// at a time (parallel trainers serialise on a mutex, oracle/rl_plans.cpp).
 class ShardCostService {
  public:
   template <class Tables, class WorkloadT>
