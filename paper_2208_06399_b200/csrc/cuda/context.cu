@@ -436,14 +436,11 @@ void EmbContext::setup_runtime() {
 
   // Index staging is small: carve out just enough shared memory for the
   // resident CTAs and leave the rest of the unified 228 KB to L1 (hot rows).
+  // The carveout is a per-function, process-wide attribute: every launch
+  // re-applies its context's (set_carveout), so contexts with other lane
+  // layouts in the same process — subset contexts retargeted to other
+  // shards — never run on a too-small carveout (fewer resident CTAs).
   {
-    const double need = (double)std::max(ASB_SEG_MINBLOCKS_FWD, ASB_SEG_MINBLOCKS_BWD) * (double)(seg_smem_bytes_ + 1024);
-    const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)) + 1);
-    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct),
-               "carveout");
-    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    pct),
-               "carveout");
     // index staging of 1-lane groups can pass the 48 KB default (any subset's kinds)
     int max_stage = 0;
     for (int k = 0; k < kNumKinds; ++k) max_stage = std::max(max_stage, stage_x_ints(k) + ((stage_s_ints(k) + 3) & ~3));
@@ -452,10 +449,6 @@ void EmbContext::setup_runtime() {
                "seg smem");
     cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn),
                "seg smem");
-    const double need_b = (double)ASB_SEG_MINBLOCKS_BWD * (double)(seg_smem_bytes_ + 1024);
-    const int pct_b = std::min(100, (int)std::ceil(100.0 * need_b / (228.0 * 1024.0)) + 1);
-    cuda_check(cudaFuncSetAttribute(seg_reduce_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct_b),
-               "carveout");
   }
   {
     // the side stream runs K2 beside the forward gather; ASB_SIDE_PRIO (A/B):
@@ -1006,10 +999,28 @@ SegParams EmbContext::seg_params(bool fwd) const {
   return p;
 }
 
+// Shared-memory carveout of the segment kernels for THIS context's staging
+// size (process-wide attribute, re-applied only when it changes).
+void EmbContext::set_carveout(bool fwd) {
+  static std::mutex mu;
+  static int last[3] = {-1, -1, -1};  // fwd fp32, fwd fp16, bwd
+  const int blocks = fwd ? ASB_SEG_MINBLOCKS_FWD : ASB_SEG_MINBLOCKS_BWD;
+  const double need = (double)blocks * (double)(seg_smem_bytes_ + 1024);
+  const int pct = std::min(100, (int)std::ceil(100.0 * need / (228.0 * 1024.0)) + 1);
+  const int which = fwd ? (w_half_ ? 1 : 0) : 2;
+  std::lock_guard<std::mutex> lk(mu);
+  if (last[which] == pct) return;
+  const void* f = fwd ? (w_half_ ? (const void*)seg_reduce_kernel<true, true> : (const void*)seg_reduce_kernel<true>)
+                      : (const void*)seg_reduce_kernel<false>;
+  cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct), "carveout");
+  last[which] = pct;
+}
+
 // K1 / K3 launch: one warp per unit, every lane layout in one launch.
 template <bool FWD>
 void EmbContext::launch_seg(SegParams p, cudaStream_t s) {
   if (n_units_ == 0) return;
+  set_carveout(FWD);
   p.unit_begin = 0;
   if (FWD && w_half_)
     seg_reduce_kernel<true, true><<<grid_for(n_units_, kWarpsPerBlock), kBlock, seg_smem_bytes_, s>>>(p);

@@ -85,6 +85,7 @@ class EmbContext {
   void launch_sort(cudaStream_t s, cudaEvent_t k4_done = nullptr);
   void layout_tables();
   void setup_runtime();
+  void set_carveout(bool fwd);
   struct Slot;
   Slot& stage_layout(const int64_t* n_idx);
   void stage_fill_host(Slot& sl, const int64_t* const* offsets, const int64_t* const* indices, const int64_t* n_idx);
