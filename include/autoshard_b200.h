@@ -196,7 +196,10 @@ AS_API as_status as_retarget_subset(as_ctx* ctx, const int32_t* positions, int32
 /* Load one batch of streams (host int64 CSR per table, ctx table order,
  * TableStream layout tables.hpp:43-47). Host memory is borrowed for the call
  * only. Validation reproduces load_workload's checks (workload_io.hpp:216-241)
- * on the device and reports OffsetError / IndexError naming the table.
+ * on the library's host staging threads while they narrow the streams to the
+ * device format (opt-in: part of the index pieces narrowed and checked on the
+ * device, ASB_RAW_EIGHTHS) and reports OffsetError / IndexError naming the
+ * table, the same first error either way.
  * stream: a cudaStream_t (NULL = legacy default). Synchronises. */
 AS_API as_status as_load_streams(as_ctx* ctx, const int64_t* const* offsets,
                                  const int64_t* const* indices, const int64_t* n_indices,
