@@ -209,6 +209,9 @@ void* EmbContext::dalloc(size_t bytes) {
 // by the caller).
 void EmbContext::layout_tables() {
   const int n = T_;
+  if ((int64_t)n * B_ >= (1LL << 31))
+    fail(AS_SHAPE, "as_create: n_tables x batch_size = " + std::to_string((int64_t)n * B_) +
+                       " bags; a shard takes at most 2^31-1 (int32 bag offsets)");
   htabs_.assign(static_cast<size_t>(n), DevTable{});
   for (int t = 0; t < n; ++t) {
     const as_table_spec& s = specs_[t];

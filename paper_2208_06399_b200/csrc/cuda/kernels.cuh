@@ -978,15 +978,26 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
                                                          const DevTable* __restrict__ tabs,
                                                          int* __restrict__ bag, float* __restrict__ out,
                                                          long long out_stride, PeerOut peers) {
+#ifdef ASB_K4_OLD
   const long long nb = (long long)T * B;
   const long long w0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
   if (w0 >= nb) return;
   const int lane = threadIdx.x & 31;
   const long long gb = min(w0 + lane, nb - 1);  // lanes past the end repeat the last bag
-  const int o = __ldg(off + gb);
-  const int e = __ldg(off + gb + 1);
   const int t = (int)(gb / B);
   const int b = (int)(gb - (long long)t * B);
+#else
+  // T*B + 1 offsets are int32-indexed (staging): 32-bit bag arithmetic
+  const int nb = T * B;
+  const int w0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+  if (w0 >= nb) return;
+  const int lane = threadIdx.x & 31;
+  const int gb = min(w0 + lane, nb - 1);  // lanes past the end repeat the last bag
+  const int t = gb / B;
+  const int b = gb - t * B;
+#endif
+  const int o = __ldg(off + gb);
+  const int e = __ldg(off + gb + 1);
   const int first = __shfl_sync(0xffffffffu, o, 0);
   const int last = __shfl_sync(0xffffffffu, e, 31);
   for (int base = first; base < last; base += 32) {
@@ -1002,7 +1013,19 @@ __global__ void __launch_bounds__(256) bag_expand_kernel(const int* __restrict__
     if (j < last) bag[j] = bj;
   }
   if (out == nullptr) return;  // ids only (backward without a forward of this batch)
+#ifdef ASB_K4_OLD
   unsigned empty = __ballot_sync(0xffffffffu, w0 + lane < nb && o == e);
+#else
+  // zero rows of empty bags: rows of <= 32 floats by their own lane (all
+  // empty bags of the warp at once), wider rows by the whole warp
+  const bool is_empty = w0 + lane < nb && o == e;
+  const int nv_mine = is_empty ? (__ldg(&tabs[t].dim) >> 2) : 0;
+  if (is_empty && nv_mine <= 8) {
+    float* row = pooled_row(out, out_stride, peers, b) + __ldg(&tabs[t].col);
+    for (int cv = 0; cv < nv_mine; ++cv) st4_streaming(row + cv * 4, make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+  unsigned empty = __ballot_sync(0xffffffffu, is_empty && nv_mine > 8);
+#endif
   while (empty) {
     const int i = __ffs(empty) - 1;
     empty &= empty - 1;
