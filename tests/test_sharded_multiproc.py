@@ -206,3 +206,22 @@ def test_cpp_dropin_example_on_gpu(cuda):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "gpu  ms:" in r.stdout, r.stdout
+
+
+def test_bench_two_ranks_one_gpu(cuda):
+    """bench.py's N > 1 path end to end (torchrun, 2 ranks): the sharded step
+    through the C-ABI, the exchange timings, the e2e loop and the JSON line.
+    Both ranks share cuda:0 (ASB_TEST_ONE_GPU=1: gloo control plane, peer
+    exchange between the two processes on one device) — a functional check of
+    the scaling run's code path, never a timing."""
+    port = _port()
+    env = dict(os.environ, ASB_TEST_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--workload", "cfg1"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert len(line["shard_ms_per_step"]) == 2 and line["exchange_timing"]["bwd_bytes_per_rank_max"] > 0
+    assert line["e2e"]["value"] > 0
