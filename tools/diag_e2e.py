@@ -1,4 +1,10 @@
-"""Timeline of the pipelined e2e loop (host-side timestamps per phase)."""
+"""Where the end-to-end step's time goes (cfg2, one B200): host timestamps of
+the pipelined loop bench.py's e2e runs (step / commit / stage per batch), then
+the staging path alone (narrow + validate + H2D + commit) and the device step
+alone. Used to tell a host-staging-bound e2e from a slow step.
+
+  python tools/diag_e2e.py
+"""
 import sys, time, os
 sys.path.insert(0, '.')
 import torch
