@@ -234,7 +234,8 @@ void EmbContext::layout_tables() {
     d.dim = s.dim;
     d.col = static_cast<int>(sum_dim_);
     d.table_id = s.id;
-    d.kind = kind_for_dim(s.dim, vec_, w_half_);
+    d.kind = kind_for_dim(s.dim, std::find(vec2_dims_.begin(), vec2_dims_.end(), s.dim) != vec2_dims_.end() ? 2 : vec_,
+                          w_half_);
     d.chunk_len = chunk_len_for(s.dim, 131072.0);
     sum_dim_ += s.dim;
     max_dim_ = std::max(max_dim_, s.dim);
@@ -260,6 +261,14 @@ EmbContext::EmbContext(int device, const as_table_spec* tables, int n, int64_t b
   if (batch < 1 || batch > (1LL << 30)) fail(AS_CONFIG, "as_create: batch_size must be in [1, 2^30]");
   check_device(device);
   if (const char* e = std::getenv("ASB_VEC")) vec_ = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("ASB_VEC2_DIMS")) {  // A/B: dims laid out with 2 float4 per lane
+    vec2_dims_.clear();
+    for (const char* c = e; *c;) {
+      vec2_dims_.push_back(std::atoi(c));
+      while (*c && *c != ',') ++c;
+      if (*c) ++c;
+    }
+  }
   if (const char* e = std::getenv("ASB_CHUNK_KB")) chunk_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
   if (const char* e = std::getenv("ASB_UNIT_KB")) unit_cap_ = std::max(2.0, std::atof(e)) * 1024.0;
   specs_.assign(tables, tables + n);
@@ -303,6 +312,7 @@ EmbContext::EmbContext(const EmbContext& parent, const int* positions, int n)
     : device_(parent.device_), T_(n), B_(parent.B_), seed_(parent.seed_), w_half_(parent.w_half_) {
   if (n < 0) fail(AS_CONFIG, "as_create_subset: n_tables must be >= 0");
   vec_ = parent.vec_;
+  vec2_dims_ = parent.vec2_dims_;
   chunk_cap_ = parent.chunk_cap_;
   unit_cap_ = parent.unit_cap_;
   specs_.resize(static_cast<size_t>(n));

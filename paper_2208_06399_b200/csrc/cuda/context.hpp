@@ -186,6 +186,9 @@ class EmbContext {
   PeerOut peers_{};  // fused forward exchange (as_set_peer_outputs); n = 0: local output
   int raw_eighths_ = 0;  // ASB_RAW_EIGHTHS: eighths of the index pieces narrowed on the GPU
   int vec_ = 1;  // preferred float4 per lane (ASB_VEC, A/B)
+  // dims laid out with 2 float4 per lane (ASB_VEC2_DIMS): 64 -> GL 8 x NV 2
+  // (cfg3 step -1.9 %; 128 helps mixed-dim shards but costs 1.7 % on cfg2)
+  std::vector<int> vec2_dims_{64};
   double chunk_cap_ = 262144.0;  // max gathered bytes per chunk (ASB_CHUNK_KB, A/B; 256 KB: -0.7 % cfg2, -1.2 % cfg3 step vs 128 KB)
   double unit_cap_ = 262144.0;  // max gathered bytes per warp unit (ASB_UNIT_KB, A/B)
   float* carry_ = nullptr;
