@@ -372,7 +372,7 @@ def main():
         lay = a2a_layout(task, plan, B)
         modes = {"peer": 0, "peer-fwd": 2, "nccl": 3}
         mode = modes[args.exchange] if not one_gpu else 0
-        comm = connect(shard, lay, rank, world, mode=mode, use_nccl=not one_gpu)
+        comm = connect(shard, lay, rank, world, mode=mode, use_nccl=not one_gpu, host_barrier=one_gpu)
         exchange = {
             0: "forward fused into K4/K1 epilogues (NVLink peer stores into the owners' receive buffers) + "
                "system-scope device barrier; backward: gradient blocks pushed to the table owners by copy engines "

@@ -336,6 +336,17 @@ AS_API as_status as_alltoall_handle(as_comm* comm, void* blob_out, int64_t* nbyt
  * peers' buffers (cudaIpcOpenMemHandle, peer access enabled lazily) and
  * points this ctx's forward at the owners' receive blocks. */
 AS_API as_status as_alltoall_open(as_comm* comm, const void* all_blobs);
+/* Host-side exchange barrier, for ranks that SHARE one device (functional
+ * tests on a 1-GPU box). The device barrier is a kernel that waits for the
+ * other ranks' arrival; kernels of different processes on one GPU are not
+ * guaranteed to run at the same time, so there it would rely on time-slicing.
+ * With fn set, the barrier instead synchronises the stream (this rank's peer
+ * stores and pushes are complete) and calls fn(user), which must return 0 once
+ * every rank has called it for this barrier (MPI_Barrier, a gloo barrier, a
+ * file rendezvous ...), non-zero on failure (-> AS_NCCL). fn == NULL restores
+ * the device barrier. */
+typedef int32_t (*as_host_barrier_fn)(void* user);
+AS_API as_status as_alltoall_host_barrier(as_comm* comm, as_host_barrier_fn fn, void* user);
 
 /* The sharded forward: K4/K1 of this rank's tables with every pooled row
  * delivered to its sample owner, then the exchange barrier (AS_XCHG_PEER) or

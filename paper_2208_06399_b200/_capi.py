@@ -149,6 +149,7 @@ SIGNATURES = {
     "as_alltoall_setup": (i32, [vp, P(i64), P(i64), i32]),
     "as_alltoall_handle": (i32, [vp, vp, P(i64)]),
     "as_alltoall_open": (i32, [vp, vp]),
+    "as_alltoall_host_barrier": (i32, [vp, vp, vp]),
     "as_forward_sharded": (i32, [vp, vp]),
     "as_backward_sharded": (i32, [vp, vp, f32, f32, vp]),
     "as_step_sharded": (i32, [vp, f32, f32, P(f64), vp]),

@@ -627,6 +627,13 @@ AS_API as_status as_alltoall_open(as_comm* comm, const void* all) {
   });
 }
 
+AS_API as_status as_alltoall_host_barrier(as_comm* comm, as_host_barrier_fn fn, void* user) {
+  return guard([&] {
+    need(comm, "comm");
+    comm->impl->set_host_barrier(fn, user);
+  });
+}
+
 AS_API as_status as_forward_sharded(as_comm* comm, void* stream) {
   return guard([&] {
     need(comm, "comm");

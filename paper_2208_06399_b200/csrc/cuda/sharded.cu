@@ -338,6 +338,15 @@ void ShardComm::check_async() {
 }
 
 void ShardComm::barrier(cudaStream_t s) {
+  if (host_fn_) {
+    // ranks on one device: nothing guarantees that two processes' kernels run
+    // at the same time, so no kernel may wait on another rank. Our peer
+    // stores / pushes complete with the stream; the host barrier then orders
+    // every rank's completed writes before anyone's next launch.
+    cuda_check(cudaStreamSynchronize(s), "host barrier: drain");
+    if (host_fn_(host_user_) != 0) fail(AS_NCCL, "host barrier callback failed; the exchange is broken");
+    return;
+  }
   BarrierFlags f;
   std::memset(&f, 0, sizeof f);
   for (int q = 0; q < world_; ++q) f.peer[q] = peer_flags_[q];

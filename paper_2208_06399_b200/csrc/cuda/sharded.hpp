@@ -35,6 +35,11 @@ class ShardComm {
   void load_exchanged(int n_all, const as_table_spec* all, const int32_t* owner, const int64_t* const* local_offsets,
                       const int64_t* const* local_indices, cudaStream_t s);
   void profile_read(double* ms2, bool reset);
+  // ranks sharing ONE device: a host-side barrier instead of the device one
+  void set_host_barrier(as_host_barrier_fn fn, void* user) {
+    host_fn_ = fn;
+    host_user_ = user;
+  }
 
  private:
   void require_open(const char* what) const;
@@ -60,6 +65,8 @@ class ShardComm {
   unsigned long long* peer_flags_[kMaxPeers] = {};
   bool opened_[kMaxPeers] = {};
   unsigned long long epoch_ = 0;
+  as_host_barrier_fn host_fn_ = nullptr;
+  void* host_user_ = nullptr;
   int* err_ = nullptr;   // device: barrier timeout
   int* h_err_ = nullptr; // pinned mirror (copied after every barrier)
   double* loss_ = nullptr;

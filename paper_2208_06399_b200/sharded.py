@@ -206,6 +206,22 @@ class ShardComm:
         allb = b"".join(bytes(b).ljust(HANDLE_BYTES, b"\0")[:HANDLE_BYTES] for b in blobs)
         self._check(self._lib().as_alltoall_open(self._h, C.create_string_buffer(allb, len(allb))))
 
+    def use_host_barrier(self, group=None) -> None:
+        """Ranks sharing ONE device (as_alltoall_host_barrier): the exchange
+        barrier becomes stream sync + torch.distributed.barrier(group) on the
+        host, so no kernel ever waits on another rank's kernel."""
+        import torch.distributed as dist
+
+        def _bar(_user):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:
+                return 1
+
+        self._host_cb = C.CFUNCTYPE(C.c_int32, C.c_void_p)(_bar)  # kept alive with the comm
+        self._check(self._lib().as_alltoall_host_barrier(self._h, C.cast(self._host_cb, C.c_void_p), None))
+
     def load_exchanged(self, all_tables: Sequence[TableDesc], owner: Sequence[int], local_streams, stream=None) -> None:
         """KJT all-to-all (as_load_streams_exchanged): local_streams
         = this rank's mini-batch, (offsets over its own rows, indices) for EVERY
@@ -284,10 +300,12 @@ class ShardComm:
 
 
 def connect(shard, layout: A2ALayout, rank: int, world: int, mode: int = XCHG_PEER, group=None,
-            use_nccl: bool = True) -> ShardComm:
+            use_nccl: bool = True, host_barrier: bool = False) -> ShardComm:
     """Build this rank's ShardComm with torch.distributed as the control plane:
     the NCCL unique id (if use_nccl) is broadcast from rank 0; without NCCL
-    the peer-memory handle blobs are all-gathered here instead of over NCCL."""
+    the peer-memory handle blobs are all-gathered here instead of over NCCL.
+    host_barrier: the ranks share one device — exchange barriers on the host
+    (ShardComm.use_host_barrier), never a device-side wait."""
     import torch.distributed as dist
 
     uid = None
@@ -301,4 +319,6 @@ def connect(shard, layout: A2ALayout, rank: int, world: int, mode: int = XCHG_PE
         blobs = [None] * world
         dist.all_gather_object(blobs, comm.handle(), group=group)
         comm.open(blobs)
+    if host_barrier:
+        comm.use_host_barrier(group)
     return comm

@@ -2,8 +2,9 @@
 // (include/autoshard_b200.h): one process per rank, no Python, no torch, no
 // MPI. The peer-memory handle blobs are exchanged through files in a shared
 // directory (any launcher's control plane would do); with one GPU both ranks
-// run on device 0 (cudaIpc between processes on one device), with several
-// rank r uses device r.
+// run on device 0 (cudaIpc between processes on one device; the exchange
+// barrier then runs on the host through files), with several rank r uses
+// device r.
 //
 //   env: RANK, WORLD (1..8), XDIR (shared directory), ASB_DEVICE (default RANK)
 //   prints: "rank R loss L0 L1 L2" — the loss 1/2|recv|^2 of this rank's
@@ -40,6 +41,19 @@ static void file_barrier(const std::string& dir, const char* tag, int rank, int 
       std::this_thread::sleep_for(std::chrono::milliseconds(5));
     }
   }
+}
+
+// Ranks sharing one device (ASB_DEVICE set): the exchange barrier runs on the
+// host (as_alltoall_host_barrier) — no kernel waits on another process's kernel.
+struct HostBarrier {
+  std::string dir;
+  int rank, world, epoch;
+};
+static int32_t host_barrier(void* user) {
+  HostBarrier* h = static_cast<HostBarrier*>(user);
+  const std::string tag = "x" + std::to_string(h->epoch++);
+  file_barrier(h->dir, tag.c_str(), h->rank, h->world);
+  return 0;
 }
 
 int main() {
@@ -92,6 +106,8 @@ int main() {
     std::ifstream(dir + "/blob_" + std::to_string(q), std::ios::binary).read(&all[(size_t)q * AS_HANDLE_BYTES],
                                                                              AS_HANDLE_BYTES);
   check(as_alltoall_open(comm, all.data()), "as_alltoall_open");
+  HostBarrier hb{dir, rank, world, 0};
+  if (std::getenv("ASB_DEVICE")) check(as_alltoall_host_barrier(comm, host_barrier, &hb), "as_alltoall_host_barrier");
 
   double loss[3];
   for (double& l : loss) check(as_step_sharded(comm, 0.01f, 1e-8f, &l, nullptr), "as_step_sharded");

@@ -43,7 +43,8 @@ def main():
     out = {"rank": rank, "ok": True, "errors": []}
     with P.EmbeddingShard(mine, B, device=dev, weight_seed=SEED) as sh:
         sh.load(wl)
-        comm = connect(sh, lay, rank, world, mode=mode, use_nccl=use_nccl)
+        comm = connect(sh, lay, rank, world, mode=mode, use_nccl=use_nccl,
+                       host_barrier=os.environ.get("ASB_ONE_GPU") == "1")
         loss = comm.step(LR, EPS, want_loss=True)
         torch.cuda.synchronize()
         recv = comm.recv_tensor().cpu().numpy()

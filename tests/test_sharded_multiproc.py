@@ -4,8 +4,11 @@ fp64 oracle of all tables (tests/sharded_worker.py).
 
 * 2 processes on ONE GPU (the GPU box has one): the peer-memory exchange
   (cudaIpc-mapped receive / gradient buffers, the fused peer-store forward, the
-  system-scope device barrier, the gradient push) between two processes —
-  NCCL refuses two ranks on one device, so the handles go over gloo.
+  gradient push) between two processes — NCCL refuses two ranks on one device,
+  so the handles go over gloo, and the exchange barrier runs on the host
+  (as_alltoall_host_barrier): kernels of two processes on one GPU are not
+  guaranteed to be co-scheduled, so no kernel may wait on the other rank. The
+  device barrier kernel runs with >= 2 GPUs.
 * >= 2 GPUs: the same with NCCL as the control plane, for every exchange mode.
 * world 1 with a real NCCL communicator (one GPU): NCCL send/recv in both
   directions must give bit-identical results to the unsharded step.

@@ -1,14 +1,15 @@
 #!/bin/bash
-# One measurement pass on a GPU box (run under gpurun): bench lines, launch
-# lists and ncu --set full summaries of ONE step's kernels, tagged $1 (e.g. r2v3).
+# One measurement pass on a GPU box (run under gpurun), tagged $1 (e.g. r2n):
+# ncu launch lists and `ncu --set full` summaries of ONE step's kernels FIRST,
+# so profiles/ncu_traffic.json carries the DRAM bytes of these very sources
+# when the bench lines are taken (bench.py reports them as roofline.traffic
+# only when the sources sha matches); then the bench lines, the GPU tests,
+# smoke() and (SANITIZE=1) compute-sanitizer.
 # The .ncu-rep files stay on the box unless KEEP_REP=1 (gpurun copies back <= 64 MiB).
 tag=${1:-run}
 set -x
+mkdir -p gpurun_out
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
-timeout 300 python bench.py > gpurun_out/${tag}_bench_cfg2.json 2> gpurun_out/${tag}_bench_cfg2.err
-timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${tag}_bench_ref.json 2>&1
-timeout 300 python bench.py --workload cfg4 --no-cpu > gpurun_out/${tag}_bench_cfg4.json 2> gpurun_out/${tag}_bench_cfg4.err
-timeout 300 python bench.py --workload cfg3 --no-cpu --no-e2e > gpurun_out/${tag}_bench_cfg3.json 2>&1
 # kernels per step: K4 + 3 sort kernels per digit pass (3 passes: tables up to 2^24 rows) + K1 + 3 fixups + K3 + 3 fixups
 N=18
 for w in cfg2 cfg4; do
@@ -23,4 +24,17 @@ for w in cfg2 cfg4; do
   python tools/ncu_summary.py /tmp/prof_${tag}_$w.ncu-rep gpurun_out/${tag}_ncu_full_$w.txt $w > /dev/null 2>&1
   [ "$KEEP_REP" = 1 ] && cp /tmp/prof_${tag}_$w.ncu-rep gpurun_out/
 done
+# the bench lines read the traffic of this capture
+cp gpurun_out/ncu_traffic.json profiles/ncu_traffic.json
+timeout 300 python bench.py > gpurun_out/${tag}_bench_cfg2.json 2> gpurun_out/${tag}_bench_cfg2.err
+timeout 300 python bench.py --impl reference > gpurun_out/${tag}_bench_ref.json 2>&1
+timeout 300 python bench.py --workload cfg4 --no-cpu > gpurun_out/${tag}_bench_cfg4.json 2> gpurun_out/${tag}_bench_cfg4.err
+timeout 300 python bench.py --workload cfg3 --no-cpu --no-e2e > gpurun_out/${tag}_bench_cfg3.json 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q -rs > gpurun_out/${tag}_pytest_gpu.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${tag}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${tag}_smoke.log 2>&1
+if [ "$SANITIZE" = 1 ]; then
+  bash tools/sanitize.sh
+  for t in memcheck racecheck synccheck initcheck; do mv gpurun_out/sanitize_$t.log gpurun_out/${tag}_sanitize_$t.log; done
+fi
 ls -la gpurun_out
