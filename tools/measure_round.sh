@@ -3,8 +3,9 @@
 # ncu launch lists and `ncu --set full` summaries of ONE step's kernels FIRST,
 # so profiles/ncu_traffic.json carries the DRAM bytes of these very sources
 # when the bench lines are taken (bench.py reports them as roofline.traffic
-# only when the sources sha matches); then the bench lines, the GPU tests,
-# smoke() and (SANITIZE=1) compute-sanitizer.
+# only when the sources sha matches); then the bench lines, the GPU tests and
+# smoke(). compute-sanitizer runs in calls of its own (tools/sanitize.sh, one
+# tool per call).
 # The .ncu-rep files stay on the box unless KEEP_REP=1 (gpurun copies back <= 64 MiB).
 tag=${1:-run}
 set -x
@@ -33,8 +34,4 @@ timeout 300 python bench.py --workload cfg3 --no-cpu --no-e2e > gpurun_out/${tag
 timeout 1500 python -m pytest tests -m gpu -x -q -rs > gpurun_out/${tag}_pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${tag}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${tag}_smoke.log 2>&1
-if [ "$SANITIZE" = 1 ]; then
-  bash tools/sanitize.sh
-  for t in memcheck racecheck synccheck initcheck; do mv gpurun_out/sanitize_$t.log gpurun_out/${tag}_sanitize_$t.log; done
-fi
 ls -la gpurun_out
