@@ -14,12 +14,15 @@ cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
 # kernels per step: K4 + 3 sort kernels per digit pass (3 passes: tables up to 2^24 rows) + K1 + 3 fixups + K3 + 3 fixups
 N=18
 for w in cfg2 cfg4; do
+  # each command under ncu has just exited 0 without it (B200_PROFILING.md)
+  timeout 300 python bench.py --workload $w --steps 2 --warmup 3 --profile-only > gpurun_out/${tag}_plain_$w.log 2>&1 &&
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches_$w.csv \
     python bench.py --workload $w --steps 2 --warmup 3 --profile-only > /dev/null 2>&1
   python tools/launch_summary.py gpurun_out/${tag}_launches_$w.csv gpurun_out/${tag}_launches_$w.txt \
     "ncu --metrics gpu__time_duration.sum --clock-control none: python bench.py --workload $w --steps 2 --warmup 3 --profile-only" > /dev/null
   rm -f gpurun_out/${tag}_launches_$w.csv
   # one whole step (the 4th, after 3 warm-up steps)
+  timeout 300 python bench.py --workload $w --steps 1 --warmup 3 --profile-only > gpurun_out/${tag}_plain1_$w.log 2>&1 &&
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"seg_|sort_|bag_expand" -s $((3 * N)) -c $N \
     -o /tmp/prof_${tag}_$w python bench.py --workload $w --steps 1 --warmup 3 --profile-only > gpurun_out/${tag}_ncu_$w.log 2>&1
   python tools/ncu_summary.py /tmp/prof_${tag}_$w.ncu-rep gpurun_out/${tag}_ncu_full_$w.txt $w > /dev/null 2>&1
