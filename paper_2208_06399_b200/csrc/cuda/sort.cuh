@@ -72,10 +72,23 @@ __device__ __forceinline__ SortView sort_view(const SortParams& sp, const DevTab
 
 // Digit position of this pass in the keys it reads: packed tables carry
 // (row << bag_bits | bag) after pass 0, whose input is the plain row.
+// Digit width of a table: its ceil(bits / 8) passes split its row bits
+// evenly (a 17-bit table sorts 6 + 6 + 5 bits, not 8 + 8 + 1), so every pass
+// has at most 2^width buckets: longer runs per bucket and tile in the
+// write-out (fewer partial sectors), fewer distinct digits per warp to rank.
+__device__ __forceinline__ int sort_width(const DevTable& tb) {
+#ifdef ASB_SORT_FULL_DIGITS
+  return kSortBits;
+#else
+  const int np = sort_passes_of(tb.sort_bits);
+  return (tb.sort_bits + np - 1) / np;
+#endif
+}
 __device__ __forceinline__ int sort_shift(const SortParams& sp, const DevTable& tb, bool as_read) {
   const bool packed_in = tb.sort_packed && (sp.pass > 0 || !as_read);
-  return sp.pass * kSortBits + (packed_in ? sp.bag_bits : 0);
+  return sp.pass * sort_width(tb) + (packed_in ? sp.bag_bits : 0);
 }
+__device__ __forceinline__ unsigned sort_mask(const DevTable& tb) { return (1u << sort_width(tb)) - 1u; }
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -96,6 +109,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_upsweep_kernel(SortParams s
   const long long lo = (long long)(sb - tb.sort_tile_off) * sp.sb_elems;
   const int n = (int)min((long long)sp.sb_elems, tb.n_lookups - lo);
   const int shift = sort_shift(sp, tb, true);
+  const unsigned dm = sort_mask(tb);
   const unsigned* k = v.kin + lo;
   __syncthreads();
   int* hw = h[warp];
@@ -109,7 +123,7 @@ __global__ void __launch_bounds__(kSortThreads) sort_upsweep_kernel(SortParams s
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (j0 + u * kSortThreads + (int)threadIdx.x < n) atomicAdd(hw + ((x[u] >> shift) & (kSortDigits - 1)), 1);
+      if (j0 + u * kSortThreads + (int)threadIdx.x < n) atomicAdd(hw + ((x[u] >> shift) & dm), 1);
   }
   __syncthreads();
   int s = 0;
@@ -184,7 +198,7 @@ struct SortSmem {
 
 template <int MODE>
 __device__ __forceinline__ void sort_downsweep_body(const SortParams& sp, SortSmem& sm, const SortView& v, int n,
-                                                    int shift) {
+                                                    int shift, unsigned dm) {
   constexpr int I = kSortItems;
   constexpr bool VALS_IN = MODE <= 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -214,7 +228,7 @@ __device__ __forceinline__ void sort_downsweep_body(const SortParams& sp, SortSm
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       const bool ok = wb + i * 32 + lane < nt;
-      const unsigned d = ok ? (key[i] >> shift) & (kSortDigits - 1) : kSortDigits + lane;
+      const unsigned d = ok ? (key[i] >> shift) & dm : kSortDigits + lane;
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int before = __popc(peers & lt);
       const int c = ok ? sm.cnt[warp][d] : 0;
@@ -254,7 +268,7 @@ __device__ __forceinline__ void sort_downsweep_body(const SortParams& sp, SortSm
 #pragma unroll
     for (int i = 0; i < I; ++i) {
       if (wb + i * 32 + lane < nt) {
-        const int lp = sm.cnt[warp][(key[i] >> shift) & (kSortDigits - 1)] + rk[i];
+        const int lp = sm.cnt[warp][(key[i] >> shift) & dm] + rk[i];
         sm.lkey[lp] = key[i];
         if constexpr (MODE == 0) sm.lval[lp] = val[i];
       }
@@ -266,7 +280,7 @@ __device__ __forceinline__ void sort_downsweep_body(const SortParams& sp, SortSm
       const int lp = i * kSortThreads + threadIdx.x;
       if (lp < nt) {
         const unsigned k = sm.lkey[lp];
-        const int pos = lp + sm.gdelta[(k >> shift) & (kSortDigits - 1)];
+        const int pos = lp + sm.gdelta[(k >> shift) & dm];
         if constexpr (MODE == 0) {
           v.kout[pos] = k;
           v.vout[pos] = sm.lval[lp];
@@ -293,13 +307,14 @@ __global__ void __launch_bounds__(kSortThreads, ASB_SORT_MINBLOCKS) sort_downswe
   v.vin += lo;
   sm.gbase[threadIdx.x] = sp.hist[(long long)sb * kSortDigits + threadIdx.x];
   const int shift = sort_shift(sp, tb, false);
+  const unsigned dm = sort_mask(tb);
   const int mode =
       !tb.sort_packed ? 0 : (sp.pass == 0 ? 1 : (sp.pass == sort_passes_of(tb.sort_bits) - 1 ? 3 : 2));
   switch (mode) {
-    case 0: sort_downsweep_body<0>(sp, sm, v, n, shift); break;
-    case 1: sort_downsweep_body<1>(sp, sm, v, n, shift); break;
-    case 2: sort_downsweep_body<2>(sp, sm, v, n, shift); break;
-    default: sort_downsweep_body<3>(sp, sm, v, n, shift); break;
+    case 0: sort_downsweep_body<0>(sp, sm, v, n, shift, dm); break;
+    case 1: sort_downsweep_body<1>(sp, sm, v, n, shift, dm); break;
+    case 2: sort_downsweep_body<2>(sp, sm, v, n, shift, dm); break;
+    default: sort_downsweep_body<3>(sp, sm, v, n, shift, dm); break;
   }
 }
 
