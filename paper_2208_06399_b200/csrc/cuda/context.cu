@@ -682,7 +682,8 @@ EmbContext::Slot& EmbContext::stage_layout(const int64_t* n_idx) {
   // K2 layout: superblocks per table; meta = [superblock -> table] then, per
   // digit pass, the superblocks of the tables that still have digits left
   {
-    // superblock = 1..16 tiles: about 6 waves of 3 CTAs per SM
+    // superblock = 1..16 tiles: about 6 waves of 3 CTAs per SM (5 are resident;
+    // sized as measured in profiles/r2_ab/r2q, r2r)
     const int64_t want = 148LL * 3 * 6;
     int sbt = 1;
     while (sbt < kSortMaxSBTiles && L / ((int64_t)kSortTile * sbt * 2) >= want) sbt *= 2;

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kSortDigits) sort_scan_kernel(SortParams sp) {
 }
 
 #ifndef ASB_SORT_MINBLOCKS
-#define ASB_SORT_MINBLOCKS 3
+#define ASB_SORT_MINBLOCKS 5
 #endif
 // Per tile: the keys and values come into registers (warp-striped: a warp
 // owns a contiguous run of the tile), are ranked stably, placed in shared

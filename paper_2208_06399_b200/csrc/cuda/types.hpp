@@ -4,7 +4,7 @@
 #include <vector_types.h>
 
 #ifndef ASB_SORT_ITEMS
-#define ASB_SORT_ITEMS 16
+#define ASB_SORT_ITEMS 8
 #endif
 
 namespace asb {
