@@ -73,6 +73,31 @@ __device__ __forceinline__ void lds_ids(const int* p, int (&x)[U]) {
     for (int i = 0; i < U; ++i) x[i] = p[i];
   }
 }
+// The same from a 32-bit shared-window address: the staged ids / keys are
+// addressed by one register per buffer instead of a generic pointer the
+// compiler re-derives from %tid and the CTA's shared window at every batch
+// (under the 64-register cap it rematerialised ~19 instructions per batch).
+__device__ __forceinline__ int lds32(unsigned a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(unsigned a, int v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+template <int U>
+__device__ __forceinline__ void lds_ids_sh(unsigned a, int (&x)[U]) {
+  if constexpr (U % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < U / 4; ++i)
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(x[4 * i]), "=r"(x[4 * i + 1]), "=r"(x[4 * i + 2]), "=r"(x[4 * i + 3])
+                   : "r"(a + 16u * i));
+  } else if constexpr (U == 2) {
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(x[0]), "=r"(x[1]) : "r"(a));
+  } else {
+#pragma unroll
+    for (int i = 0; i < U; ++i) x[i] = lds32(a + 4u * i);
+  }
+}
 __device__ __forceinline__ float f4dot(float4 a) { return a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w; }
 __device__ __forceinline__ float4 shfl4(float4 v, int src) {
   return make_float4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
@@ -354,6 +379,9 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 #endif
 }
+__device__ __forceinline__ void cp_async4_sh(unsigned s, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -446,26 +474,29 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
   const unsigned long long gpol = l2_policy_last();
 #endif
 
+  // this group's staging buffers as 32-bit shared addresses (buffer 0; +kStage*4 B for buffer 1)
+  const unsigned xsh = static_cast<unsigned>(__cvta_generic_to_shared(xs)) + 4u * (g * SR);
+  const unsigned ssh = static_cast<unsigned>(__cvta_generic_to_shared(ss)) + 4u * (g * (SR + 1));
   // stage the row ids [base, base+SR) and keys [base, base+SR] of one super-round
   auto stage = [&](EIdx base, int buf) {
-    int* gx = xs + buf * kStageX + g * SR;
-    int* gs = ss + buf * kStageS + g * (SR + 1);
+    const unsigned gx = xsh + 4u * (buf * kStageX);
+    const unsigned gs = ssh + 4u * (buf * kStageS);
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int m = q * GL + c;
       const EIdx e = base + m;
-      if (e < j_hi) cp_async4(gx + m, p.src + e);
+      if (e < j_hi) cp_async4_sh(gx + 4u * m, p.src + e);
       if (e < t_hi)
-        cp_async4(gs + m, p.seg + e);
+        cp_async4_sh(gs + 4u * m, p.seg + e);
       else
-        gs[m] = -2;
+        sts32(gs + 4u * m, -2);
     }
     if (c == 0) {
       const EIdx e = base + SR;
       if (e < t_hi)
-        cp_async4(gs + SR, p.seg + e);
+        cp_async4_sh(gs + 4u * SR, p.seg + e);
       else
-        gs[SR] = -2;
+        sts32(gs + 4u * SR, -2);
     }
     cp_async_commit();
   };
@@ -490,14 +521,15 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
       cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const int* gx = xs + buf * kStageX + g * SR;
-    const int* gs = ss + buf * kStageS + g * (SR + 1);
+    const unsigned gxa = xsh + 4u * (buf * kStageX);
+    const unsigned gsa = ssh + 4u * (buf * kStageS);
+    auto gs = [&](int k) { return lds32(gsa + 4u * k); };
     const int nval = (int)max((EIdx)0, min((EIdx)SR, j_hi - base));
     unsigned endm = 0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int m = q * GL + c;
-      const bool end = m < nval && gs[m] != gs[m + 1];
+      const bool end = m < nval && gs(m) != gs(m + 1);
       const unsigned be = __ballot_sync(0xffffffffu, end);
       endm |= ((be >> (g * GL)) & low_bits<GL>()) << (q * GL);
     }
@@ -507,7 +539,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
       unsigned ebits = (endm >> m0) & low_bits<U>();
       float4 v[U][NV];
       int ids[U];
-      lds_ids<U>(gx + m0, ids);
+      lds_ids_sh<U>(gxa + 4u * m0, ids);
       if (m0 + U <= nval) {  // full batch: no element predicate
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -552,7 +584,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #ifndef ASB_NO_NARROW_PREFETCH
         if constexpr (!FWD) {
           if (ebits) {
-            spre = gs[m0 + __ffs(ebits) - 1];
+            spre = gs(m0 + __ffs(ebits) - 1);
             if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
           }
         }
@@ -563,7 +595,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
           for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
           const bool endu = (ebits >> u) & 1u;
           if (__any_sync(0xffffffffu, endu)) {
-            const int s = gs[m0 + u];
+            const int s = gs(m0 + u);
             const bool split = s == prev_seg;
             if (endu && split) {
               store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
@@ -589,7 +621,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
       int spre = -7;
       if constexpr (!FWD) {
         if (ebits) {
-          spre = gs[m0 + __ffs(ebits) - 1];
+          spre = gs(m0 + __ffs(ebits) - 1);
           if (spre != prev_seg) load_row_state<GL, NV>(p, tb, spre, c, wpre, mpre);
         }
       }
@@ -608,7 +640,7 @@ __device__ __forceinline__ void seg_unit(const SegParams& p, const DevTable& tb,
 #pragma unroll
                 for (int w = 0; w < NV; ++w) acc[w] = f4add(acc[w], v[u][w]);
             if (e >= U) break;
-            const int s = gs[m0 + e];
+            const int s = gs(m0 + e);
             if (s == prev_seg) {
               // completes a segment that began in an earlier chunk -> fixup
               store_carry<GL, NV, PAIR>(p, chunk, 0, nvec, c, acc);
