@@ -46,11 +46,24 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
   return make_float4(lo.x, lo.y, hi.x, hi.y);
 #endif
 }
-// base + row * stride in ONE IMAD.WIDE.U32 (64-bit addend)
+// base + row * stride. ptxas splits a 64-bit-addend mad.wide.u32 into
+// IMAD.WIDE.U32 + IADD3 + IMAD.X when the base does not sit in an aligned
+// register pair; the carry-chained form (low word with carry-out, high word
+// with carry-in) is two IMADs whatever the allocation.
 __device__ __forceinline__ const char* row_addr(const char* base, unsigned row, unsigned stride) {
+#ifdef ASB_MADWIDE_ADDR
   const char* r;
   asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(row), "r"(stride), "l"(base));
   return r;
+#else
+  const unsigned long long b = reinterpret_cast<unsigned long long>(base);
+  unsigned lo, hi;
+  asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\t"
+      "madc.hi.u32 %1, %2, %3, %5;"
+      : "=r"(lo), "=r"(hi)
+      : "r"(row), "r"(stride), "r"(static_cast<unsigned>(b)), "r"(static_cast<unsigned>(b >> 32)));
+  return reinterpret_cast<const char*>((static_cast<unsigned long long>(hi) << 32) | lo);
+#endif
 }
 // U consecutive staged row ids (16-B aligned when U % 4 == 0) with vector LDS
 template <int U>
